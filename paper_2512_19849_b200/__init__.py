@@ -1,0 +1,21 @@
+"""B200-native expert-parallel dispatch/combine (arXiv 2512.19849 / UCCL-EP path).
+
+Public surface:
+* ``Buffer``, ``Config``, ``EventOverlap`` — DeepEP-compatible API
+* ``LocalGroup`` — R ranks on one GPU (single-GPU multi-rank test harness)
+* ``command``, ``imm``, ``kernels``, ``fifo`` — drop-ins for the reference's
+  epsim.command / epsim.imm / epsim.kernels and the FifoChannel of SPEC.md:17-124
+* ``per_token_cast_to_fp8`` — the LL FP8 quantiser as a standalone op
+
+Everything executes in libepb200.so (csrc/); importing fails loudly if the
+library has not been built.
+"""
+from . import _lib  # noqa: F401  (loads libepb200.so or raises)
+from .buffer import Buffer, Config, EventOverlap, LocalGroup, nvl_bytes_hint
+from .errors import (ChannelShutdown, ConfigError, ConnectionError_, EpsimError, FaultError, InvariantViolation,
+                     ProtocolViolation, RingDeadlock, UnsupportedOperation)
+from .ops import per_token_cast_to_fp8
+
+__all__ = ["Buffer", "Config", "EventOverlap", "LocalGroup", "nvl_bytes_hint", "per_token_cast_to_fp8",
+           "EpsimError", "ProtocolViolation", "ChannelShutdown", "ConfigError", "FaultError", "ConnectionError_",
+           "UnsupportedOperation", "InvariantViolation", "RingDeadlock"]

@@ -1,0 +1,155 @@
+// api.cpp — context lifecycle, CUDA-IPC bootstrap and error plumbing of the
+// C ABI (include/epb.h).  Replaces the reference's symmetric-region handshake
+// ("exchanges the base address during handshake",
+// PAPER.md:326-327) with CUDA IPC handles: each rank cudaMalloc's one region,
+// exports its handle, and maps every peer's region into its address space so
+// kernels can store straight into peer memory over NVLink.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "ctx.h"
+
+static thread_local std::string g_last_error;
+
+int epb_set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int epb_cuda_check(cudaError_t e, const char* what) {
+  return epb_set_error(EPB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+extern "C" const char* epb_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int epb_num_sms(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return n;
+}
+
+int epb_fifo_init(epb_ctx* ctx);     // proxy.cpp
+void epb_fifo_free(epb_ctx* ctx);    // proxy.cpp
+
+extern "C" int epb_create(epb_t** out, int rank, int world, const epb_config_t* cfg) {
+  if (!out || !cfg) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
+  *out = nullptr;
+  if (world <= 0 || world > epb::kMaxRanks) return epb_set_error(EPB_ERR_CONFIG, "world size must be in [1, 8]");
+  if (rank < 0 || rank >= world) return epb_set_error(EPB_ERR_CONFIG, "rank out of range");
+  if (cfg->fifo_channels < 0 || cfg->fifo_channels > 64)
+    return epb_set_error(EPB_ERR_CONFIG, "fifo_channels must be in [0, 64] (6-bit channel_id, command.py:37)");
+  if (cfg->fifo_channels > 0 && (cfg->fifo_capacity <= 0 || (cfg->fifo_capacity & (cfg->fifo_capacity - 1))))
+    return epb_set_error(EPB_ERR_CONFIG, "fifo_capacity must be a power of two (SPEC.md:108)");
+  epb_ctx* ctx = new epb_ctx();
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->cfg = *cfg;
+  if (ctx->cfg.num_recv_slots <= 0) ctx->cfg.num_recv_slots = 2;
+  if (const char* s = std::getenv("EPB_TIMEOUT_S")) ctx->timeout_ns = (uint64_t)(std::atof(s) * 1e9);
+  cudaError_t e = cudaGetDevice(&ctx->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  ctx->region_bytes = epb::kRegionHeader + epb::align_up(cfg->nvl_bytes, 4096) + epb::align_up(cfg->ll_bytes, 4096);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->base, ctx->region_bytes);
+  if (e == cudaSuccess) e = cudaMemset(ctx->base, 0, ctx->region_bytes);
+  if (e == cudaSuccess) e = cudaHostAlloc(&ctx->host, sizeof(epb::HostInfo), cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    std::memset((void*)ctx->host, 0, sizeof(epb::HostInfo));
+    e = cudaHostGetDevicePointer((void**)&ctx->host_dev, (void*)ctx->host, 0);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    int rc = epb_cuda_check(e, "epb_create");
+    if (ctx->base) cudaFree(ctx->base);
+    if (ctx->host) cudaFreeHost((void*)ctx->host);
+    delete ctx;
+    return rc;
+  }
+  ctx->peer[rank] = ctx->base;
+  if (int rc = epb_fifo_init(ctx)) {
+    cudaFree(ctx->base);
+    cudaFreeHost((void*)ctx->host);
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return EPB_OK;
+}
+
+extern "C" int epb_proxy_stop(epb_t* ctx);
+
+extern "C" int epb_destroy(epb_t* ctx) {
+  if (!ctx) return EPB_OK;
+  cudaDeviceSynchronize();
+  epb_proxy_stop(ctx);
+  epb_fifo_free(ctx);
+  for (int r = 0; r < ctx->world; ++r)
+    if (ctx->peer_ipc[r] && ctx->peer[r]) cudaIpcCloseMemHandle(ctx->peer[r]);
+  if (ctx->base) cudaFree(ctx->base);
+  if (ctx->host) cudaFreeHost((void*)ctx->host);
+  delete ctx;
+  return EPB_OK;
+}
+
+extern "C" int epb_ipc_handle(epb_t* ctx, void* out_handle) {
+  if (!ctx || !out_handle) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == EPB_IPC_HANDLE_BYTES, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  EPB_CUDA(cudaIpcGetMemHandle(&h, ctx->base));
+  std::memcpy(out_handle, &h, sizeof(h));
+  return EPB_OK;
+}
+
+extern "C" int epb_open_peers(epb_t* ctx, const void* handles) {
+  if (!ctx || !handles) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
+  const char* hb = static_cast<const char*>(handles);
+  for (int r = 0; r < ctx->world; ++r) {
+    if (r == ctx->rank || ctx->peer[r]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hb + (size_t)r * EPB_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return epb_set_error(EPB_ERR_CONNECTION, std::string("cudaIpcOpenMemHandle(rank ") +
+                                                                         std::to_string(r) + "): " +
+                                                                         cudaGetErrorString(e));
+    ctx->peer[r] = static_cast<char*>(p);
+    ctx->peer_ipc[r] = true;
+  }
+  return EPB_OK;
+}
+
+extern "C" int epb_link_local(epb_t* const* ctxs, int n) {
+  if (!ctxs || n <= 0 || n > epb::kMaxLocal) return epb_set_error(EPB_ERR_PROTOCOL, "bad local group");
+  for (int i = 0; i < n; ++i) {
+    if (!ctxs[i] || ctxs[i]->world != n || ctxs[i]->rank != i)
+      return epb_set_error(EPB_ERR_CONFIG, "local group must hold ranks 0..n-1 of a world of n");
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) ctxs[i]->peer[j] = ctxs[j]->base;
+  return EPB_OK;
+}
+
+extern "C" int epb_device_error(epb_t* ctx, int64_t* detail) {
+  if (!ctx) return epb_set_error(EPB_ERR_PROTOCOL, "null context");
+  if (detail) *detail = ctx->host->err_detail;
+  return (int)ctx->host->err_code;
+}
+
+extern "C" int epb_clear_device_error(epb_t* ctx) {
+  if (!ctx) return epb_set_error(EPB_ERR_PROTOCOL, "null context");
+  ctx->host->err_code = 0;
+  ctx->host->err_detail = 0;
+  return EPB_OK;
+}
+
+extern "C" int epb_region(epb_t* ctx, void** base, size_t* bytes) {
+  if (!ctx) return epb_set_error(EPB_ERR_PROTOCOL, "null context");
+  if (base) *base = ctx->base;
+  if (bytes) *bytes = ctx->region_bytes;
+  return EPB_OK;
+}

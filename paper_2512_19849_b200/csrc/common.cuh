@@ -1,0 +1,211 @@
+// common.cuh — shared device/host definitions for the sm_100a EP kernels.
+//
+// Memory model used throughout ("release/acquire discipline"):
+//   * payload rows go to peer memory with plain 16-byte stores (NVLink posted
+//     writes), then every writer thread executes fence.sc.sys and the block
+//     barrier orders all of them before ONE st.release.sys / red.release.sys
+//     on the peer's flag/counter;
+//   * receivers spin with ld.acquire.sys on their own flag words, then a
+//     block barrier publishes the observation to the rest of the block.
+// This replaces the reference ring's plain loads/stores (kernels.py:5-8,
+// kernels.py:67-79), which rely on x86-TSO and do not carry over to a
+// GPU <-> peer / GPU <-> host channel.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "../../include/epb.h"
+
+namespace epb {
+
+constexpr int kMaxRanks = EPB_MAX_RANKS;
+constexpr int kMaxLocal = EPB_MAX_LOCAL;
+constexpr int kMaxChannels = EPB_MAX_CHANNELS;
+constexpr int kMaxLocalExperts = EPB_MAX_LOCAL_EXPERTS;
+constexpr int kMaxFifo = 64;  // 6-bit channel_id (command.py:37)
+
+// ---------------------------------------------------------------------------
+// Symmetric-region layout (identical offsets on every rank).
+//   [0, kMetaBytes)                 Meta: flags/counters/mailboxes peers write
+//   [kMetaBytes, kRegionHeader)     Scratch: this rank's private plan words
+//   [kRegionHeader, +nvl_bytes)     normal-mode arena (recv slots + staging)
+//   [.., +ll_bytes)                 low-latency region
+// ---------------------------------------------------------------------------
+struct NotifyMsg {                       // one source rank's dispatch counts
+  int32_t counts_per_rank[kMaxRanks];    // src's num_tokens_per_rank
+  int32_t slot;                          // src's receive slot (where peers write TO src)
+  int32_t num_tokens;                    // src's T
+  int32_t pad[2];
+  int32_t channel_counts[kMaxChannels];  // src's tokens to me, per channel
+  int32_t expert_counts[kMaxLocalExperts];  // src's tokens for each of my local experts
+};
+
+struct Meta {
+  uint32_t mbox_flag[2][kMaxRanks];      // epoch stamp of mbox[parity][src]
+  uint32_t disp_done[kMaxRanks];         // += 1 per dispatch block of src (monotonic)
+  uint32_t comb_done[kMaxRanks];         // += 1 per combine block of src (monotonic)
+  uint64_t ll_disp_flag[2][kMaxRanks];   // LL dispatch: epoch stamp per src
+  uint64_t ll_comb_flag[2][kMaxRanks];   // LL combine: epoch stamp per src
+  uint32_t barrier[kMaxRanks];
+  uint32_t pad[24];
+  uint64_t proxy_sig[kMaxFifo][kMaxRanks];  // CPU-proxy signals: += 1 per piggybacked WRITE from src on channel
+  NotifyMsg mbox[2][kMaxRanks];
+};
+
+struct Scratch {                         // private to the owning rank
+  uint64_t dst_rows[kMaxRanks];          // peer VA of dst's recv slot (this call)
+  int32_t row_base[kMaxRanks];           // my first row inside dst's slot
+  int32_t abort;                         // notify detected an error: skip data path
+  int32_t pad0;
+  uint32_t ll_ticket[4];                 // LL last-warp tickets: [dispatch|combine][parity]
+  // GPU -> CPU FIFOs: control arrays live in pinned host memory; the producer
+  // keeps its tail (and a cached head) here, in device memory.
+  uint64_t fifo_ctl[kMaxFifo];           // device aliases of the pinned ctl arrays
+  int64_t fifo_tail[kMaxFifo];
+  int64_t fifo_head[kMaxFifo];
+  int32_t fifo_channels;
+  int32_t fifo_cap;
+};
+
+constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+constexpr size_t kMetaBytes = align_up(sizeof(Meta), 4096);
+constexpr size_t kScratchBytes = align_up(sizeof(Scratch), 4096);
+constexpr size_t kRegionHeader = kMetaBytes + kScratchBytes;
+
+// Pinned, device-mapped host words the kernels publish to the CPU.
+struct HostInfo {
+  volatile int64_t notify_epoch;
+  volatile int64_t num_recv;
+  volatile int64_t err_code;
+  volatile int64_t err_detail;
+  volatile int32_t recv_per_expert[kMaxLocalExperts];
+};
+
+// What a kernel needs to know about one (possibly emulated) rank.
+struct RankView {
+  int rank, world;
+  char* base;                  // my region
+  char* peer[kMaxRanks];       // every rank's region, mapped in this process
+  HostInfo* host;              // device alias of the pinned HostInfo
+  uint64_t timeout_ns;
+};
+
+__host__ __device__ inline Meta* meta_of(char* base) { return reinterpret_cast<Meta*>(base); }
+__host__ __device__ inline Scratch* scratch_of(char* base) { return reinterpret_cast<Scratch*>(base + kMetaBytes); }
+
+// ---------------------------------------------------------------------------
+// PTX helpers (sm_100a).
+// ---------------------------------------------------------------------------
+#ifdef __CUDACC__
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(int64_t* p, int64_t v) {
+  asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int64_t ld_volatile(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.volatile.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// 16-byte streaming loads/stores.  Source rows are read once: keep them out
+// of L1.  Peer stores are plain st.global (they leave the SM as NVLink writes).
+__device__ __forceinline__ int4 ld_nc_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int4 ld_cg_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(int4* p, const int4& v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_na_v4(int4* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Record an error into the host-visible word (first error wins is not
+// required: any non-zero code makes the host raise).
+__device__ __forceinline__ void report_error(const RankView& rv, int code, int64_t detail) {
+  rv.host->err_detail = detail;
+  rv.host->err_code = code;
+  scratch_of(rv.base)->abort = code;
+  __threadfence_system();
+}
+
+// Spin until *p >= target (wrap-safe for monotonically increasing u32
+// counters).  Returns false on timeout after reporting EPB_ERR_DEADLOCK.
+__device__ __forceinline__ bool wait_geq(const RankView& rv, const uint32_t* p, uint32_t target, int64_t tag) {
+  uint64_t t0 = 0;
+  int iter = 0;
+  while (static_cast<int32_t>(ld_acquire_sys(p) - target) < 0) {
+    if ((++iter & 1023) == 0) {
+      uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > rv.timeout_ns) {
+        report_error(rv, EPB_ERR_DEADLOCK, tag);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+__device__ __forceinline__ bool wait_geq64(const RankView& rv, const uint64_t* p, uint64_t target, int64_t tag) {
+  uint64_t t0 = 0;
+  int iter = 0;
+  while (static_cast<int64_t>(ld_acquire_sys(p) - target) < 0) {
+    if ((++iter & 1023) == 0) {
+      uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > rv.timeout_ns) {
+        report_error(rv, EPB_ERR_DEADLOCK, tag);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+#endif  // __CUDACC__
+
+}  // namespace epb

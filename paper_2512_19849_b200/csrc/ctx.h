@@ -1,0 +1,57 @@
+// ctx.h — host-side state of one EP rank (the object behind epb_t*).
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+struct epb_proxy;  // proxy.cpp
+
+struct epb_ctx {
+  int rank = 0, world = 1, device = 0;
+  epb_config_t cfg{};
+  size_t region_bytes = 0;
+  char* base = nullptr;                 // cudaMalloc'd symmetric region
+  char* peer[epb::kMaxRanks] = {};      // mapped peer regions (peer[rank] == base)
+  bool peer_ipc[epb::kMaxRanks] = {};   // opened with cudaIpcOpenMemHandle
+  epb::HostInfo* host = nullptr;        // pinned host view
+  epb::HostInfo* host_dev = nullptr;    // device alias
+  uint32_t disp_epoch = 0, comb_epoch = 0, ll_disp_epoch = 0, ll_comb_epoch = 0;
+  uint32_t disp_cum = 0, comb_cum = 0;  // cumulative expected block signals per source
+  uint64_t ll_proxy_disp = 0, ll_proxy_comb = 0;  // proxy-transport LL calls so far (signal targets)
+  int num_sms = 148;
+  uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;
+  // LL bookkeeping of the last dispatch (shape) for combine validation.
+  int ll_last_tokens = -1;
+  // GPU -> CPU command FIFOs (pinned, mapped) and the proxy.
+  std::vector<int64_t*> fifo_host;      // ctl arrays (kernels.py:23-31 layout)
+  std::vector<int64_t*> fifo_dev;       // device aliases
+  epb_proxy* proxy = nullptr;
+
+  size_t arena_off() const { return epb::kRegionHeader; }
+  size_t ll_off() const { return epb::kRegionHeader + epb::align_up(cfg.nvl_bytes, 4096); }
+
+  epb::RankView view() const {
+    epb::RankView v{};
+    v.rank = rank;
+    v.world = world;
+    v.base = base;
+    for (int i = 0; i < epb::kMaxRanks; ++i) v.peer[i] = peer[i];
+    v.host = host_dev;
+    v.timeout_ns = timeout_ns;
+    return v;
+  }
+};
+
+// error plumbing (api.cpp)
+int epb_set_error(int code, const std::string& msg);
+int epb_cuda_check(cudaError_t e, const char* what);
+#define EPB_CUDA(call)                                              \
+  do {                                                              \
+    cudaError_t _e = (call);                                        \
+    if (_e != cudaSuccess) return epb_cuda_check(_e, #call);        \
+  } while (0)
