@@ -1,0 +1,439 @@
+"""Benchmark of the EP dispatch/combine hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1 runs in-process; N > 1 is launched by the driver under torchrun (one
+process per GPU, NCCL only for the start/stop barrier and the max-over-ranks
+reduction of the timings; the data path itself uses no collective).
+
+Workload (BASELINE.json configs[1]): DeepSeek-V3 normal mode, 4096 tokens per
+rank, hidden 7168, 256 experts, top-8, bf16 dispatch / bf16 combine, EP = N.
+A step = get_dispatch_layout -> dispatch -> combine through the public Buffer
+API, on synthetic seeded inputs already resident in HBM.  Four input sets
+rotate so every step's inputs (4 x 58.7 MB) were evicted from the 126 MB L2.
+
+value = payload bytes moved per step by all ranks (dispatch rows + combine
+rows, every (token, destination-rank) row counted once per direction, local
+rows included) / step time, in GB/s.  `roofline` describes the dominant
+kernel (HBM-bound at EP=1, NVLink-bound at EP>1).
+`e2e` repeats the step from pinned host buffers (H2D of x/topk/weights, D2H of
+the combined output) through the same API.  `ll` reports the low-latency
+128-token FP8 dispatch + bf16 combine in microseconds (direct NVLink stores
+and the GPU->CPU FIFO proxy transport).  `cpu_baseline` times the oracle port
+on the box's host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+T_PER_RANK, HIDDEN, EXPERTS, TOPK = 4096, 7168, 256, 8
+LL_TOKENS = 128
+ROW = HIDDEN * 2
+WORKLOAD = "DeepSeek-V3 normal mode: 4096 tok/rank, hidden 7168, 256 experts, top-8, bf16 dispatch + bf16 combine"
+METRIC = "dispatch/combine GB/s per GPU at 1/2/4/8 B200 (+ LL µs) vs NVLink roofline"
+NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); no NVLink entry in MEASURED_PEAKS
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """SM clock / throttle-reason sampler (NVML, every ~2 ms) running during the
+    timed region — the same counters `nvidia-smi --query-gpu=clocks.sm,...,
+    clocks_event_reasons.*` reports, at a rate that fits millisecond regions."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.stop = threading.Event()
+        self.h = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception:
+            self.h = None
+        return self
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        try:
+            reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.samples.append((sm, reasons))
+
+    def _run(self):
+        while not self.stop.is_set():
+            self._sample()
+            time.sleep(0.002)
+
+    def __exit__(self, *exc):
+        if self.h is not None:
+            self.stop.set()
+            self.t.join(timeout=2)
+            self._sample()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for _, r in self.samples for bit, name in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(self.samples), "source": "NVML during the timed region"}
+
+
+# ----------------------------------------------------------------------------------
+# CPU reference arm (the oracle port; /root/reference does not exist on the GPU box)
+# ----------------------------------------------------------------------------------
+def _cpu_inputs(rank: int, T: int):
+    from tests.helpers import bf16_random, make_routing
+    g = np.random.default_rng(1000 + rank)
+    idx, w = make_routing(g, T, EXPERTS, TOPK)
+    x = bf16_random(g, (T, HIDDEN))
+    return x, idx, w
+
+
+def _cpu_step(x, idx, w, world, threads):
+    """Oracle layout -> dispatch -> combine for one rank's tokens at EP=world (the
+    local view: rows to every destination, and the same rows combined back)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import ep as O
+    T = x.shape[0]
+    chunks = np.array_split(np.arange(T), threads)
+
+    def part(tok):
+        xs = x[tok]
+        in_rank = O.get_dispatch_layout(idx[tok], EXPERTS, world)[2]
+        out, heads = O.dispatch([xs] + [xs[:0]] * (world - 1), [in_rank] + [in_rank[:0]] * (world - 1))
+        comb = O.combine([o["recv_x"] for o in out], [in_rank] + [in_rank[:0]] * (world - 1), heads,
+                         out[0]["rank_prefix_matrix"])
+        return int(in_rank.sum()), comb[0][0]
+    with ThreadPoolExecutor(threads) as ex:
+        res = list(ex.map(part, chunks))
+    rows = sum(r[0] for r in res)
+    return rows
+
+
+def cpu_baseline(world: int, budget_s: float = 12.0, threads: int = 1):
+    x, idx, w = _cpu_inputs(0, T_PER_RANK)
+    _cpu_step(x, idx, w, world, threads)  # warm
+    t0 = time.perf_counter()
+    n, rows = 0, 0
+    while time.perf_counter() - t0 < budget_s or n == 0:
+        rows += _cpu_step(x, idx, w, world, threads)
+        n += 1
+    dt = time.perf_counter() - t0
+    gbs = 2 * rows * ROW / dt / 1e9
+    return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{n} full steps (layout+dispatch+combine of 4096x7168 bf16 tokens, EP={world} local view) "
+                      f"in {dt:.1f} s with the numpy oracle"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = args.gpus
+    threads = max(1, len(os.sched_getaffinity(0)))
+    x, idx, w = _cpu_inputs(0, T_PER_RANK)
+    for _ in range(args.warmup):
+        _cpu_step(x, idx, w, world, threads)
+    t0 = time.perf_counter()
+    rows = 0
+    for _ in range(args.steps):
+        rows += _cpu_step(x, idx, w, world, threads)
+    dt = time.perf_counter() - t0
+    gbs = 2 * rows * ROW / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded routing, N(0,1) bf16 tokens)",
+            "config": {"workload": WORKLOAD, "ep": world, "tokens_per_rank": T_PER_RANK, "hidden": HIDDEN,
+                       "experts": EXPERTS, "topk": TOPK, "parallelism": f"ep{world}"},
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                             "sample": f"{args.steps} timed steps of rank 0's 4096-token workload (oracle numpy "
+                                       f"port of the reference path, {threads} threads)"},
+            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    group = None
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        group = dist.group.WORLD
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+
+    import paper_2512_19849_b200 as epb
+    from tests.helpers import bf16_random, make_routing
+
+    R = world
+    dev = torch.device("cuda", local_rank)
+    nvl = epb.nvl_bytes_hint(T_PER_RANK, HIDDEN, R, TOPK, 3)
+    ll_bytes = epb.Buffer.get_low_latency_rdma_size_hint(LL_TOKENS, HIDDEN, R, EXPERTS, num_topk=TOPK)
+    buf = epb.Buffer(group, nvl, ll_bytes, low_latency_mode=True, fifo_channels=16, fifo_capacity=1024,
+                     proxy_threads=4, ll_transport="nvlink")
+
+    # rotating input sets (4 x 58.7 MB > 126 MB L2)
+    NSETS = 4
+    sets = []
+    for i in range(NSETS):
+        g = np.random.default_rng(10_000 * rank + i)
+        idx, w = make_routing(g, T_PER_RANK, EXPERTS, TOPK)
+        x = bf16_random(g, (T_PER_RANK, HIDDEN))
+        sets.append((torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev),
+                     torch.from_numpy(idx).to(dev), torch.from_numpy(w).to(dev)))
+    # payload rows this rank moves per step (dispatch rows = combine rows)
+    rows, remote_rows = [], []
+    for x, idx, w in sets:
+        m = torch.zeros(T_PER_RANK, R, dtype=torch.bool, device=dev)
+        m.scatter_(1, idx // (EXPERTS // R), True)  # routing has no masked entries
+        rows.append(int(m.sum()))
+        m[:, rank] = False
+        remote_rows.append(int(m.sum()))
+
+    def step(i):
+        x, idx, w = sets[i % NSETS]
+        per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(idx, EXPERTS)
+        recv_x, rti, rtw, _, handle, _ = buf.dispatch(x, num_tokens_per_rank=per_rank, is_token_in_rank=in_rank,
+                                                      num_tokens_per_expert=per_exp, topk_idx=idx, topk_weights=w)
+        out, out_w, _ = buf.combine(recv_x, handle, topk_weights=rtw)
+        return out
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    for i in range(max(3, args.warmup)):
+        step(i)
+    barrier()
+
+    # ---- timed region (device events) -----------------------------------------------
+    buf._g.prof = []
+    clocks = Clocks(local_rank)
+    with clocks:
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for i in range(args.steps):
+            step(i)
+        ev1.record()
+        barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    prof = buf._g.prof
+    buf._g.prof = None
+    per_kernel = {}
+    for name, s, e in prof:
+        per_kernel.setdefault(name, []).append(s.elapsed_time(e))
+    ms = max_over_ranks(ms_local)
+    my_rows = sum(rows[i % NSETS] for i in range(args.steps))
+    my_remote = sum(remote_rows[i % NSETS] for i in range(args.steps))
+    job_bytes = sum_over_ranks(2.0 * my_rows * ROW)
+    value = job_bytes / (ms / 1e3) / 1e9
+    ms_per_step = ms / args.steps
+    launches_per_step = 4  # layout, notify, dispatch, combine
+
+    # ---- roofline of the dominant kernel -------------------------------------------------
+    hbm_peak, peak_kind = _peaks()
+    avg = {k: statistics.mean(v) for k, v in per_kernel.items()}
+    dom = max(("dispatch", "combine"), key=lambda k: avg.get(k, 0.0))
+    steps_rows = my_rows / args.steps
+    steps_remote = my_remote / args.steps
+    if R == 1:
+        algo = 2.0 * steps_rows * ROW  # read source rows + write destination rows
+        bound, peak, unit = "hbm", hbm_peak, "GB/s"
+    else:
+        algo = steps_remote * ROW  # unique payload bytes leaving this rank over NVLink
+        bound, peak, unit = "nvlink", NVLINK_PEAK_GBS, "GB/s"
+    achieved = algo / (avg[dom] / 1e3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(f"{dom}_ep{R}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": bound, "kernel": dom, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind if R == 1 else
+                "B200_PROFILING.md measured peer copy (770 GB/s/direction)",
+                "algorithmic_bytes_per_launch": int(algo), "avg_launch_ms": round(avg[dom], 4)}
+    kernels_ms = {k: round(v, 4) for k, v in avg.items()}
+
+    # ---- end to end from pinned host buffers ---------------------------------------------
+    hx = [s[0].cpu().pin_memory() for s in sets]
+    hidx = [s[1].cpu().pin_memory() for s in sets]
+    hw = [s[2].cpu().pin_memory() for s in sets]
+    hout = torch.empty((T_PER_RANK, HIDDEN), dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step(i):
+        j = i % NSETS
+        x = hx[j].to(dev, non_blocking=True)
+        idx = hidx[j].to(dev, non_blocking=True)
+        w = hw[j].to(dev, non_blocking=True)
+        per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(idx, EXPERTS)
+        recv_x, rti, rtw, _, handle, _ = buf.dispatch(x, num_tokens_per_rank=per_rank, is_token_in_rank=in_rank,
+                                                      num_tokens_per_expert=per_exp, topk_idx=idx, topk_weights=w)
+        out, _, _ = buf.combine(recv_x, handle, topk_weights=rtw)
+        hout.copy_(out, non_blocking=True)
+
+    for i in range(3):
+        e2e_step(i)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        e2e_step(i)
+    e1.record()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    h2d = T_PER_RANK * ROW + T_PER_RANK * TOPK * 12
+    d2h = T_PER_RANK * ROW
+    e2e = {"value": round(job_bytes / (e2e_ms / 1e3) / 1e9, 4), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms / args.steps, 4)}
+
+    # ---- low-latency decode (128 tokens, FP8 dispatch + bf16 combine) ----------------------
+    ll = {}
+    for transport in (() if args.no_ll else ("nvlink", "proxy")):
+        try:
+            ll[transport] = ll_bench(buf, transport, rank, R, dev, args, barrier, max_over_ranks)
+        except Exception as exc:  # keep the headline even if a transport is unavailable
+            ll[transport] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
+    buf._g.check_device_error()
+    line = None
+    if rank == 0:
+        cpu = cpu_baseline(R) if (R == 1 and not args.no_cpu_baseline) else None
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": R, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded uniform top-8 routing, N(0,1) bf16 tokens)",
+                "config": {"workload": WORKLOAD, "ep": R, "tokens_per_rank": T_PER_RANK, "hidden": HIDDEN,
+                           "experts": EXPERTS, "topk": TOPK, "parallelism": f"ep{R}",
+                           "l2": f"{NSETS} rotating input sets ({NSETS * T_PER_RANK * ROW / 1e6:.0f} MB > 126 MB L2)"},
+                "per_gpu_gbs": round(value / R, 3),
+                "kernels_ms": kernels_ms, "roofline": roofline, "e2e": e2e, "ll_us": ll,
+                "gpu_launches": launches_per_step * args.steps, "gpu_launches_scope": "per rank",
+                "clocks": clocks.summary(), "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    buf.destroy()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def ll_bench(buf, transport, rank, R, dev, args, barrier, max_over_ranks):
+    import torch
+    from tests.helpers import bf16_random, make_routing
+    import paper_2512_19849_b200 as epb
+    from paper_2512_19849_b200._lib import check, lib
+    if transport == "proxy" and not buf._rank.proxy_running:
+        check(lib.epb_proxy_start(buf._rank.ctx))
+        buf._rank.proxy_running = True
+    buf.ll_transport = transport
+    g = np.random.default_rng(77 + rank)
+    idx, w = make_routing(g, LL_TOKENS, EXPERTS, TOPK)
+    x = torch.from_numpy(bf16_random(g, (LL_TOKENS, HIDDEN)).view(np.int16)).view(torch.bfloat16).to(dev)
+    idx_t = torch.from_numpy(idx).to(dev)
+    w_t = torch.from_numpy(w).to(dev)
+    L = EXPERTS // R
+    y = torch.randn(L, R * LL_TOKENS, HIDDEN, device=dev).to(torch.bfloat16)
+
+    def once():
+        recv, count, handle, _, _ = buf.low_latency_dispatch(x, idx_t, LL_TOKENS, EXPERTS, use_fp8=True)
+        out, _, _ = buf.low_latency_combine(y, idx_t, w_t, handle)
+        return out
+
+    for _ in range(5):
+        once()
+    barrier()
+    n = max(20, args.steps)
+    buf._g.prof = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n):
+        once()
+    e1.record()
+    barrier()
+    prof = buf._g.prof
+    buf._g.prof = None
+    d_us = statistics.median([s.elapsed_time(e) for k, s, e in prof if k == "ll_dispatch"]) * 1e3
+    c_us = statistics.median([s.elapsed_time(e) for k, s, e in prof if k == "ll_combine"]) * 1e3
+    tot = max_over_ranks(e0.elapsed_time(e1) / n * 1e3)
+    buf.ll_transport = "nvlink"
+    return {"dispatch_us": round(max_over_ranks(d_us), 2), "combine_us": round(max_over_ranks(c_us), 2),
+            "step_us": round(tot, 2), "tokens": LL_TOKENS, "fp8": True}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ll", action="store_true", help="skip the low-latency sub-benchmarks (e.g. under ncu)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -189,6 +189,19 @@ class _Group:
         self.world = ranks[0].world
         self.timeout_s = _DEFAULT_TIMEOUT_S
         self._ctxs = _ctx_array(ranks)
+        # optional per-launch CUDA-event records [(name, start, end)] for benchmarks
+        self.prof: Optional[list] = None
+
+    def _launch(self, name: str, fn) -> None:
+        if self.prof is None:
+            check(fn())
+            return
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        check(fn())
+        e.record()
+        self.prof.append((name, s, e))
 
     # -- layout ------------------------------------------------------------
     def get_dispatch_layout(self, topk_idx_list: Sequence[torch.Tensor], num_experts: int):
@@ -203,8 +216,8 @@ class _Group:
             per_rank = torch.empty(self.world, dtype=torch.int32, device=dev)
             per_expert = torch.empty(num_experts, dtype=torch.int32, device=dev)
             in_rank = torch.empty((T, self.world), dtype=torch.bool, device=dev)
-            check(lib.epb_get_dispatch_layout(ptr(topk_idx), T, k, num_experts, self.world, ptr(per_rank),
-                                              ptr(per_expert), ptr(in_rank), stream))
+            self._launch("layout", lambda: lib.epb_get_dispatch_layout(
+                ptr(topk_idx), T, k, num_experts, self.world, ptr(per_rank), ptr(per_expert), ptr(in_rank), stream))
             out.append((per_rank, None, per_expert, in_rank))
         return out
 
@@ -268,8 +281,11 @@ class _Group:
                                        copy_out=copy_out, rpm=rpm, cpm=cpm, rcpm=rcpm, send_head=send_head,
                                        in_rank=in_rank, topk_idx=topk_idx, topk_weights=topk_weights))
         try:
-            check(lib.epb_notify_dispatch(self._ctxs, n, args, C_, stream))
-            results = []
+            self._launch("notify", lambda: lib.epb_notify_dispatch(self._ctxs, n, args, C_, stream))
+            # the dispatch kernel reads its plan (peer slots, row bases) from device
+            # memory written by notify, so it is enqueued before the host waits for
+            # the receive counts; if notify flagged an error the kernel moves no data
+            self._launch("dispatch", lambda: lib.epb_dispatch(self._ctxs, n, args, C_, stream))
             for i, rk in enumerate(self.ranks):
                 st = per_rank_state[i]
                 Lx = st["E"] // R if st["E"] else 0
@@ -278,12 +294,12 @@ class _Group:
                 check(lib.epb_wait_notify(rk.ctx, C.byref(nrecv), per_exp if Lx else None, Lx, self.timeout_s))
                 st["num_recv"] = nrecv.value
                 st["per_expert_list"] = [int(per_exp[j]) for j in range(Lx)] if Lx else None
-            check(lib.epb_dispatch(self._ctxs, n, args, C_, stream))
         except Exception:
             for st, rk in zip(per_rank_state, self.ranks):
                 if not st["copy_out"]:
                     rk._release_slot(st["slot"])
             raise
+        results = []
         for i, rk in enumerate(self.ranks):
             st = per_rank_state[i]
             lay, N, H, k = st["lay"], st["num_recv"], st["H"], st["k"]
@@ -343,7 +359,7 @@ class _Group:
             a.num_tokens, a.combined_x, a.combined_topk_weights = T, ptr(out), ptr(out_w)
             keep.append((x, w))
             outs.append((out, out_w))
-        check(lib.epb_combine(self._ctxs, n, args, cfg.resolved_sms(), stream))
+        self._launch("combine", lambda: lib.epb_combine(self._ctxs, n, args, cfg.resolved_sms(), stream))
         return outs
 
     # -- low latency -------------------------------------------------------
@@ -390,7 +406,7 @@ class _Group:
             handle = (src_info, layout_range, Tm, H, num_experts, route, comb_slot, count, k, bool(use_proxy))
             recv = (packed_x, packed_s.transpose(1, 2)) if use_fp8 else packed_x
             res.append((recv, count, handle))
-        check(lib.epb_ll_dispatch(self._ctxs, n, args, _device_sms(), stream))
+        self._launch("ll_dispatch", lambda: lib.epb_ll_dispatch(self._ctxs, n, args, _device_sms(), stream))
         hook = None
         if return_recv_hook:
             def hook(args=args, keep=keep):
@@ -427,7 +443,7 @@ class _Group:
             a.use_proxy = int(use_proxy)
             keep.append((x, topk_idx, w))
             res.append(out)
-        check(lib.epb_ll_combine(self._ctxs, n, args, _device_sms(), stream))
+        self._launch("ll_combine", lambda: lib.epb_ll_combine(self._ctxs, n, args, _device_sms(), stream))
         hook = None
         if return_recv_hook:
             def hook(args=args, keep=keep):

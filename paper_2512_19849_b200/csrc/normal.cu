@@ -66,6 +66,29 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(const int64_t* _
     if (s_hist[E + i]) atomicAdd(&per_rank[i], s_hist[E + i]);
 }
 
+// Inclusive scan of n <= 32*k ints in shared memory by one warp; writes the
+// scanned row to `out` (global) and returns the total.
+__device__ __forceinline__ int warp_inclusive_scan_row(const int32_t* in, int32_t* out, int n, int lane) {
+  const int per = (n + 31) / 32, base = lane * per;
+  int local = 0;
+  for (int i = 0; i < per; ++i)
+    if (base + i < n) local += in[base + i];
+  int incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  int run = incl - local;
+  for (int i = 0; i < per; ++i) {
+    if (base + i < n) {
+      run += in[base + i];
+      out[base + i] = run;
+    }
+  }
+  return __shfl_sync(0xffffffffu, incl, 31);
+}
+
 // ---------------------------------------------------------------------------
 // notify: one block per (local) rank.
 // ---------------------------------------------------------------------------
@@ -91,23 +114,33 @@ __global__ void __launch_bounds__(kNotifyThreads, 1) notify_kernel(const __grid_
   __shared__ int32_t s_tot[kMaxRanks];
   __shared__ int32_t s_rpm[kMaxRanks][kMaxRanks];
 
-  // 1. my per-(destination, channel) token counts; channel c = tokens [c*Tc, (c+1)*Tc)
+  // 1. my per-(destination, channel) token counts; channel c = tokens [c*Tc, (c+1)*Tc).
+  //    Warp per channel, lanes over tokens, per-destination counts reduced with __reduce_add_sync.
   const int Tc = (T + C - 1) / C;
-  for (int p = tid; p < R * C; p += nthr) {
-    const int d = p % R, c = p / R;
+  const int nwarps = nthr >> 5;
+  for (int c = warp; c < C; c += nwarps) {
     const int t0 = c * Tc, t1 = min(T, t0 + Tc);
-    int n = 0;
-    for (int t = t0; t < t1; ++t) n += a.is_token_in_rank[(size_t)t * R + d] != 0;
-    s_cnt[d][c] = n;
+    int n[kMaxRanks];
+#pragma unroll
+    for (int d = 0; d < kMaxRanks; ++d) n[d] = 0;
+    for (int t = t0 + lane; t < t1; t += 32) {
+      const uint8_t* row = a.is_token_in_rank + (size_t)t * R;
+#pragma unroll
+      for (int d = 0; d < kMaxRanks; ++d)
+        if (d < R) n[d] += row[d] != 0;
+    }
+#pragma unroll
+    for (int d = 0; d < kMaxRanks; ++d) {
+      if (d < R) {
+        const int tot = __reduce_add_sync(0xffffffffu, n[d]);
+        if (lane == 0) s_cnt[d][c] = tot;
+      }
+    }
   }
   __syncthreads();
-  if (tid < R) {
-    int run = 0;
-    for (int c = 0; c < C; ++c) {
-      run += s_cnt[tid][c];
-      a.channel_prefix_matrix[tid * C + c] = run;
-    }
-    s_tot[tid] = run;
+  if (warp < R) {
+    const int tot = warp_inclusive_scan_row(&s_cnt[warp][0], a.channel_prefix_matrix + warp * C, C, lane);
+    if (lane == 0) s_tot[warp] = tot;
   }
   __syncthreads();
 
@@ -134,21 +167,20 @@ __global__ void __launch_bounds__(kNotifyThreads, 1) notify_kernel(const __grid_
   if (tid < R) wait_geq(rv, &my->mbox_flag[par][tid], epoch, 0x100 + tid);
   __syncthreads();
 
-  // 4. prefix sums
-  if (tid < R) {
-    const int d = tid;
+  // 4. prefix sums: stage every source's counts in shared memory (parallel loads),
+  //    then warp scans (no serial chains of global loads).
+  for (int i = tid; i < R * C; i += nthr) s_cnt[i / C][i % C] = __ldcg(&my->mbox[par][i / C].channel_counts[i % C]);
+  if (tid < R * R) s_rpm[tid / R][tid % R] = __ldcg(&my->mbox[par][tid / R].counts_per_rank[tid % R]);
+  __syncthreads();
+  if (warp < R) {
+    warp_inclusive_scan_row(&s_cnt[warp][0], a.recv_channel_prefix_matrix + warp * C, C, lane);
+  } else if (warp == R && lane < R) {
+    const int d = lane;  // inclusive prefix over source rank, column d
     int run = 0;
     for (int s = 0; s < R; ++s) {
-      run += __ldcg(&my->mbox[par][s].counts_per_rank[d]);
+      run += s_rpm[s][d];
       s_rpm[s][d] = run;
       a.rank_prefix_matrix[s * R + d] = run;
-    }
-  } else if (tid >= 32 && tid < 32 + R) {
-    const int s = tid - 32;
-    int run = 0;
-    for (int c = 0; c < C; ++c) {
-      run += __ldcg(&my->mbox[par][s].channel_counts[c]);
-      a.recv_channel_prefix_matrix[s * C + c] = run;
     }
   }
   if (a.num_tokens_per_expert != nullptr) {
@@ -346,6 +378,44 @@ __device__ __forceinline__ int4 pack_bf16x8(const float* acc) {
   return r;
 }
 
+// Sum NV bf16 rows in order into one bf16 row.  Each lane keeps NV*U 16-byte
+// loads in flight (U columns per lane per step, NV*U <= 8) so a warp has
+// >= 4 KB outstanding whatever the fan-in; accumulation is fp32 with one
+// rounding to bf16 at the end (canonical order).
+template <int NV>
+__device__ __forceinline__ void reduce_rows(const int4* const* rows, int4* out, int n16, int lane) {
+  constexpr int U = NV >= 8 ? 1 : 8 / NV;
+  const int4* r[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) r[j] = rows[j];
+  for (int base = lane; base < n16; base += 32 * U) {
+    int4 v[U][NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + 32 * u;
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (i < n16) v[u][j] = ld_cg_v4(r[j] + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + 32 * u;
+      if (i < n16) {
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) acc_bf16x8(acc, v[u][j]);
+        st_na_v4(out + i, pack_bf16x8(acc));
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void zero_row(int4* out, int n16, int lane) {
+  for (int i = lane; i < n16; i += 32) st_na_v4(out + i, make_int4(0, 0, 0, 0));
+}
+
 __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __grid_constant__ CombineParams P) {
   const int lr = blockIdx.y;
   const RankView& rv = P.rv[lr];
@@ -451,18 +521,24 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
       }
     }
     int4* out = reinterpret_cast<int4*>(static_cast<char*>(a.combined_x) + (size_t)t * row_bytes);
-    for (int i = lane; i < n16; i += 32) {
-      int4 v[kMaxRanks];
+    // compact the contributing rows in ascending rank order (the canonical sum order)
+    const int4* cr[kMaxRanks];
+    int nv = 0;
 #pragma unroll
-      for (int d = 0; d < kMaxRanks; ++d)
-        if (rows[d] != nullptr) v[d] = self_row[d] ? ld_nc_v4(rows[d] + i) : ld_cg_v4(rows[d] + i);
-      float acc[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
-#pragma unroll
-      for (int d = 0; d < kMaxRanks; ++d)
-        if (rows[d] != nullptr) acc_bf16x8(acc, v[d]);
-      st_na_v4(out + i, pack_bf16x8(acc));
+    for (int d = 0; d < kMaxRanks; ++d) {
+      cr[d] = nullptr;
+      if (rows[d] != nullptr) cr[nv++] = rows[d];
+    }
+    switch (nv) {
+      case 1: reduce_rows<1>(cr, out, n16, lane); break;
+      case 2: reduce_rows<2>(cr, out, n16, lane); break;
+      case 3: reduce_rows<3>(cr, out, n16, lane); break;
+      case 4: reduce_rows<4>(cr, out, n16, lane); break;
+      case 5: reduce_rows<5>(cr, out, n16, lane); break;
+      case 6: reduce_rows<6>(cr, out, n16, lane); break;
+      case 7: reduce_rows<7>(cr, out, n16, lane); break;
+      case 8: reduce_rows<8>(cr, out, n16, lane); break;
+      default: zero_row(out, n16, lane); break;
     }
     if (a.combined_topk_weights != nullptr && lane < k) {
       float w = 0.0f;
