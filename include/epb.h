@@ -82,6 +82,8 @@ const char* epb_last_error(void);
 int epb_device_error(epb_t* ctx, int64_t* detail);
 int epb_clear_device_error(epb_t* ctx);
 int epb_num_sms(void);
+/* Phase timestamps (64 x %globaltimer ns) recorded by the kernels when EPB_TRACE=1. */
+int epb_trace(epb_t* ctx, int64_t* out64);
 /* Base device address of this rank's symmetric region and its size. */
 int epb_region(epb_t* ctx, void** base, size_t* bytes);
 
@@ -126,15 +128,15 @@ typedef struct {
   int32_t* send_head;                  /* [T, R]  row of t inside my block at r, -1 */
 } epb_dispatch_args_t;
 
-/* Count exchange + prefix sums (one cross-rank round trip). */
-int epb_notify_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_args_t* args, int num_channels,
-                        void* stream);
-/* Host wait for the notify result (pinned mapped memory). per_expert: [num_local_experts] or NULL. */
-int epb_wait_notify(epb_t* ctx, int64_t* num_recv, int32_t* num_recv_per_expert, int num_local_experts,
-                    double timeout_s);
-/* Row push into peers' recv slots over NVLink (no data-path collective call). */
+/* One cooperative launch: per-channel counts, the cross-rank count exchange
+ * (one NVLink mailbox round trip), prefix sums, then every deduplicated row
+ * pushed straight into its final row of the destination's receive slot. */
 int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_args_t* args, int num_channels,
                  void* stream);
+/* Host wait for the receive counts the dispatch kernel publishes to pinned
+ * memory mid-kernel.  per_expert: [num_local_experts] or NULL. */
+int epb_wait_notify(epb_t* ctx, int64_t* num_recv, int32_t* num_recv_per_expert, int num_local_experts,
+                    double timeout_s);
 
 typedef struct {
   const void* x;              /* [N_recv, hidden] bf16, my receive order        */

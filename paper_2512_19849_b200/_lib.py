@@ -103,9 +103,9 @@ _proto("epb_device_error", c_int, vp, P64)
 _proto("epb_clear_device_error", c_int, vp)
 _proto("epb_num_sms", c_int)
 _proto("epb_region", c_int, vp, C.POINTER(vp), C.POINTER(C.c_size_t))
+_proto("epb_trace", c_int, vp, P64)
 _proto("epb_get_dispatch_layout", c_int, vp, c_int, c_int, c_int, c_int, vp, vp, vp, vp)
 _proto("epb_recv_layout", c_int, vp, c_int, c_int, C.POINTER(RecvLayout))
-_proto("epb_notify_dispatch", c_int, CTXS, c_int, C.POINTER(DispatchArgs), c_int, vp)
 _proto("epb_wait_notify", c_int, vp, P64, P32, c_int, c_double)
 _proto("epb_dispatch", c_int, CTXS, c_int, C.POINTER(DispatchArgs), c_int, vp)
 _proto("epb_combine", c_int, CTXS, c_int, C.POINTER(CombineArgs), c_int, vp)
@@ -139,14 +139,21 @@ _proto("epb_fifo_device_bench", c_int, vp, i64, c_int, P64, vp)
 # every symbol include/epb.h declares (checked by tests/test_abi.py)
 EXPORTED = [
     "epb_create", "epb_destroy", "epb_ipc_handle", "epb_open_peers", "epb_link_local", "epb_last_error",
-    "epb_device_error", "epb_clear_device_error", "epb_num_sms", "epb_region", "epb_get_dispatch_layout",
-    "epb_recv_layout", "epb_notify_dispatch", "epb_wait_notify", "epb_dispatch", "epb_combine", "epb_ll_layout",
+    "epb_device_error", "epb_clear_device_error", "epb_num_sms", "epb_region", "epb_trace", "epb_get_dispatch_layout",
+    "epb_recv_layout", "epb_wait_notify", "epb_dispatch", "epb_combine", "epb_ll_layout",
     "epb_ll_dispatch", "epb_ll_combine", "epb_per_token_cast_to_fp8", "epb_cmd_pack", "epb_cmd_pack_fields",
     "epb_cmd_unpack_fields", "epb_imm_encode_ll_batch", "epb_imm_encode_ht_batch", "epb_ring_push_batch",
     "epb_ring_pop_batch", "epb_ring_poll", "epb_ring_mark_completed", "epb_ring_check_completion",
     "epb_ring_shutdown", "epb_apply_deliveries", "epb_fifo_ctl", "epb_proxy_start", "epb_proxy_stop",
     "epb_proxy_stats", "epb_fifo_device_bench",
 ]
+
+
+def raw_stream() -> int:
+    """cudaStream_t of torch's current stream on the current device (the cheap
+    path; torch.cuda.current_stream() costs ~10 us of Python per call)."""
+    import torch
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def check(rc: int) -> None:

@@ -21,7 +21,8 @@ OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libepb200.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3,-Wall", f"-I{ROOT / 'include'}"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3,-Wall", f"-I{ROOT / 'include'}",
+          "-Wno-deprecated-gpu-targets"]
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-O3"]
 
 
@@ -62,12 +63,38 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
     if lib_stale:
         tmp = LIB.with_suffix(".so.tmp")
         cmd = [nvcc, "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ARCH + [
-            "-cudart", "static", "-Xcompiler", "-fPIC", "-lpthread", "-ldl", "-lrt"]
+            "-cudart", "static", "-Xcompiler", "-fPIC", "-Xlinker", "-soname=libepb200.so", "-lpthread", "-ldl",
+            "-lrt"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         os.replace(tmp, LIB)
+    build_ext(force=force or lib_stale, verbose=verbose)
     return LIB
+
+
+EXT = PKG / "_epb_ext.so"
+
+
+def build_ext(force: bool = False, verbose: bool = False) -> Path:
+    """The C++ per-call host runtime (pybind11 + ATen), a client of libepb200.so.
+    It resolves libepb200.so by SONAME; _lib.py loads that library first."""
+    src = CSRC / "ext" / "epb_ext.cpp"
+    deps = [src, LIB, ROOT / "include" / "epb.h"]
+    if not force and EXT.exists() and EXT.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
+        return EXT
+    from torch.utils.cpp_extension import load
+    bdir = ROOT / "build" / "ext"
+    bdir.mkdir(parents=True, exist_ok=True)
+    import ctypes
+    ctypes.CDLL(str(LIB), mode=os.RTLD_NOW | ctypes.RTLD_GLOBAL)  # so the import inside load() resolves it
+    load(name="_epb_ext", sources=[str(src)], extra_include_paths=[str(ROOT / "include")],
+         extra_cflags=["-O3", "-std=c++17"], extra_ldflags=[f"-L{PKG}", "-l:libepb200.so"],
+         build_directory=str(bdir), with_cuda=True, verbose=verbose, is_python_module=True)
+    tmp = EXT.with_suffix(".so.tmp")
+    shutil.copy(bdir / "_epb_ext.so", tmp)
+    os.replace(tmp, EXT)
+    return EXT
 
 
 if __name__ == "__main__":

@@ -52,6 +52,7 @@ extern "C" int epb_create(epb_t** out, int rank, int world, const epb_config_t* 
   ctx->cfg = *cfg;
   if (ctx->cfg.num_recv_slots <= 0) ctx->cfg.num_recv_slots = 2;
   if (const char* s = std::getenv("EPB_TIMEOUT_S")) ctx->timeout_ns = (uint64_t)(std::atof(s) * 1e9);
+  if (const char* s = std::getenv("EPB_TRACE")) ctx->trace = std::atoi(s) != 0;
   cudaError_t e = cudaGetDevice(&ctx->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
   ctx->region_bytes = epb::kRegionHeader + epb::align_up(cfg->nvl_bytes, 4096) + epb::align_up(cfg->ll_bytes, 4096);
@@ -151,5 +152,11 @@ extern "C" int epb_region(epb_t* ctx, void** base, size_t* bytes) {
   if (!ctx) return epb_set_error(EPB_ERR_PROTOCOL, "null context");
   if (base) *base = ctx->base;
   if (bytes) *bytes = ctx->region_bytes;
+  return EPB_OK;
+}
+
+extern "C" int epb_trace(epb_t* ctx, int64_t* out64) {
+  if (!ctx || !out64) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
+  EPB_CUDA(cudaMemcpy(out64, epb::scratch_of(ctx->base)->trace, sizeof(int64_t) * 64, cudaMemcpyDeviceToHost));
   return EPB_OK;
 }

@@ -1,0 +1,262 @@
+// combine.cu — normal-mode combine on sm_100a (DeepEP Buffer.combine;
+// SPEC.md:446-454 combine, PAPER.md:142 hierarchical reduce).
+//
+// One cooperative kernel: phase A pushes each received row back to its
+// source rank, into the mirror of the position the source sent it from;
+// a cross-rank counter barrier; phase B reduces every token's partials in
+// fp32 in ascending rank order (canonical order) and rounds
+// once to bf16.  Rows a rank sent to itself are read in place.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+#include "ctx.h"
+
+namespace epb {
+
+constexpr int kCombineThreads = 384;  // 12 warps; <= 168 registers/thread
+constexpr int kCopyUnroll = 7;
+// ---------------------------------------------------------------------------
+// combine: cooperative grid.  Phase A pushes each received row back into its
+// source's staging at the mirror of the dispatch position; phase B (after a
+// cross-rank counter barrier) reduces in fp32, ascending rank order, and
+// rounds once to bf16.  Rows a rank sent to itself are read from x directly.
+// ---------------------------------------------------------------------------
+struct CombineParams {
+  int n_local;
+  uint32_t epoch[kMaxLocal];
+  uint32_t expected[kMaxLocal];
+  RankView rv[kMaxLocal];
+  epb_combine_args_t a[kMaxLocal];
+  epb_recv_layout_t lay;
+};
+
+__device__ __forceinline__ void acc_bf16x8(float* acc, const int4& v) {
+  const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    acc[2 * i] = __fadd_rn(acc[2 * i], __uint_as_float(w[i] << 16));
+    acc[2 * i + 1] = __fadd_rn(acc[2 * i + 1], __uint_as_float(w[i] & 0xffff0000u));
+  }
+}
+__device__ __forceinline__ int4 pack_bf16x8(const float* acc) {
+  int4 r;
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  r.x = (int)w[0];
+  r.y = (int)w[1];
+  r.z = (int)w[2];
+  r.w = (int)w[3];
+  return r;
+}
+
+// Sum NV bf16 rows in order into one bf16 row.  Each lane keeps NV*U 16-byte
+// loads in flight (U columns per lane per step, NV*U <= 8) so a warp has
+// >= 4 KB outstanding whatever the fan-in; accumulation is fp32 with one
+// rounding to bf16 at the end (canonical order).
+struct RowSrc {
+  const char* x;      // combine input (rows this rank received from itself)
+  const char* stage;  // staging (rows pushed back by peers)
+  size_t row_bytes;
+  int me, self_base;
+  int pre[kMaxRanks];
+};
+
+template <int NV>
+__device__ __forceinline__ void reduce_rows(const RowSrc& rs, uint32_t mask, const int32_t* sh, int4* out, int n16,
+                                            int lane) {
+  constexpr int U = NV >= 8 ? 1 : 8 / NV;
+  const int4* r[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int d = __fns(mask, 0, j + 1);  // (j+1)-th contributing rank, ascending
+    const int p = sh[d];
+    r[j] = reinterpret_cast<const int4*>(d == rs.me ? rs.x + (size_t)(rs.self_base + p) * rs.row_bytes
+                                                    : rs.stage + (size_t)(rs.pre[d] + p) * rs.row_bytes);
+  }
+  for (int base = lane; base < n16; base += 32 * U) {
+    int4 v[U][NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + 32 * u;
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (i < n16) v[u][j] = ld_cg_v4(r[j] + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + 32 * u;
+      if (i < n16) {
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) acc_bf16x8(acc, v[u][j]);
+        st_na_v4(out + i, pack_bf16x8(acc));
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void zero_row(int4* out, int n16, int lane) {
+  for (int i = lane; i < n16; i += 32) st_na_v4(out + i, make_int4(0, 0, 0, 0));
+}
+
+__global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __grid_constant__ CombineParams P) {
+  const int lr = blockIdx.y;
+  const RankView& rv = P.rv[lr];
+  const epb_combine_args_t& a = P.a[lr];
+  const int R = rv.world, me = rv.rank, nb = gridDim.x, b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const uint32_t epoch = P.epoch[lr];
+  const int par = epoch & 1;
+  __shared__ int32_t s_cnt[kMaxRanks][kMaxRanks];  // count[s][d]
+  __shared__ int32_t s_excl[kMaxRanks];            // first row from s in my receive order
+  __shared__ int32_t s_sendpre[kMaxRanks];         // where my rows start in s's staging
+  __shared__ int32_t s_mypre[kMaxRanks];           // where d's rows start in my staging
+  if (tid < R * R) {
+    const int s = tid / R, d = tid % R;
+    const int* rpm = a.rank_prefix_matrix;
+    s_cnt[s][d] = rpm[s * R + d] - (s > 0 ? rpm[(s - 1) * R + d] : 0);
+  }
+  __syncthreads();
+  if (tid < R) {
+    const int s = tid;
+    s_excl[s] = s > 0 ? a.rank_prefix_matrix[(s - 1) * R + me] : 0;
+    int acc = 0;
+    for (int d = 0; d < me; ++d) acc += s_cnt[s][d];
+    s_sendpre[s] = acc;
+    acc = 0;
+    for (int d = 0; d < s; ++d) acc += s_cnt[me][d];
+    s_mypre[s] = acc;
+  }
+  __syncthreads();
+
+  const int H = a.hidden, k = a.num_topk;
+  const size_t row_bytes = (size_t)H * 2;
+  const int n16 = (int)(row_bytes >> 4);
+  const bool abort = scratch_of(rv.base)->abort != 0;
+  trace_mark(rv, 16);
+
+  // phase A: push rows back to their sources
+  const int N = a.num_recv;
+  const int Jb = (N + nb - 1) / nb;
+  const int j0 = b * Jb, j1 = min(N, j0 + Jb);
+  if (!abort) {
+    for (int j = j0 + warp; j < j1; j += nwarps) {
+      int s = 0;
+      while (s < R - 1 && j >= s_excl[s] + s_cnt[s][me]) ++s;
+      if (s == me) continue;
+      const size_t drow = (size_t)(s_sendpre[s] + (j - s_excl[s]));
+      char* stage = rv.peer[s] + P.lay.comb_off[par];
+      const int4* src = reinterpret_cast<const int4*>(static_cast<const char*>(a.x) + (size_t)j * row_bytes);
+      int4* dst = reinterpret_cast<int4*>(stage + drow * row_bytes);
+      for (int base = 0; base < n16; base += 32 * kCopyUnroll) {
+        int4 v[kCopyUnroll];
+#pragma unroll
+        for (int u = 0; u < kCopyUnroll; ++u) {
+          const int i = base + u * 32 + lane;
+          if (i < n16) v[u] = ld_nc_v4(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kCopyUnroll; ++u) {
+          const int i = base + u * 32 + lane;
+          if (i < n16) st_v4(dst + i, v[u]);
+        }
+      }
+      if (a.topk_weights != nullptr && lane < k)
+        reinterpret_cast<float*>(stage + P.lay.comb_w_off)[drow * k + lane] = a.topk_weights[(size_t)j * k + lane];
+    }
+  }
+  __syncthreads();
+  trace_mark(rv, 17);
+  if (tid < R) red_release_sys_add(&meta_of(rv.peer[tid])->comb_done[me], 1u);
+  if (tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
+  __syncthreads();
+  trace_mark(rv, 18);
+  if (abort) return;
+
+  // phase B: reduce my tokens
+  const char* my_stage = rv.base + P.lay.comb_off[par];
+  const int T = a.num_tokens;
+  const int Tb = (T + nb - 1) / nb;
+  const int tb0 = b * Tb, tb1 = min(T, tb0 + Tb);
+  RowSrc rs;
+  rs.x = static_cast<const char*>(a.x);
+  rs.stage = my_stage;
+  rs.row_bytes = row_bytes;
+  rs.me = me;
+  rs.self_base = s_excl[me];
+#pragma unroll
+  for (int d = 0; d < kMaxRanks; ++d) rs.pre[d] = s_mypre[d];
+  for (int t = tb0 + warp; t < tb1; t += nwarps) {
+    const int32_t* sh = a.send_head + (size_t)t * R;
+    // contributing ranks as a bitmask; rows are taken in ascending rank order
+    // (the canonical sum order) via __fns inside reduce_rows
+    uint32_t mask = 0;
+    if (lane < R && sh[lane] >= 0) mask = 1u << lane;
+    mask = __reduce_or_sync(0xffffffffu, mask);
+    int4* out = reinterpret_cast<int4*>(static_cast<char*>(a.combined_x) + (size_t)t * row_bytes);
+    switch (__popc(mask)) {
+      case 1: reduce_rows<1>(rs, mask, sh, out, n16, lane); break;
+      case 2: reduce_rows<2>(rs, mask, sh, out, n16, lane); break;
+      case 3: reduce_rows<3>(rs, mask, sh, out, n16, lane); break;
+      case 4: reduce_rows<4>(rs, mask, sh, out, n16, lane); break;
+      case 5: reduce_rows<5>(rs, mask, sh, out, n16, lane); break;
+      case 6: reduce_rows<6>(rs, mask, sh, out, n16, lane); break;
+      case 7: reduce_rows<7>(rs, mask, sh, out, n16, lane); break;
+      case 8: reduce_rows<8>(rs, mask, sh, out, n16, lane); break;
+      default: zero_row(out, n16, lane); break;
+    }
+    if (a.combined_topk_weights != nullptr && lane < k) {
+      float w = 0.0f;
+      for (uint32_t m = mask; m != 0; m &= m - 1) {
+        const int d = __ffs(m) - 1;
+        const int p = sh[d];
+        const float* wsrc = d == me ? a.topk_weights : reinterpret_cast<const float*>(my_stage + P.lay.comb_w_off);
+        const size_t widx = d == me ? (size_t)(rs.self_base + p) : (size_t)(rs.pre[d] + p);
+        if (wsrc != nullptr) w = __fadd_rn(w, wsrc[widx * k + lane]);
+      }
+      a.combined_topk_weights[(size_t)t * k + lane] = w;
+    }
+  }
+  trace_mark(rv, 19);
+}
+
+}  // namespace epb
+
+using namespace epb;
+
+extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_args_t* args, int num_sms,
+                           void* stream) {
+  if (int e = check_group(ctxs, n_local)) return e;
+  CombineParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.n_local = n_local;
+  int nb = std::max(1, num_sms / n_local);
+  int max_active = 0;
+  EPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_active, combine_kernel, kCombineThreads, 0));
+  nb = std::min(nb, std::max(1, max_active * ctxs[0]->num_sms / n_local));
+  for (int i = 0; i < n_local; ++i) {
+    epb_ctx* c = ctxs[i];
+    const epb_combine_args_t& a = args[i];
+    if (int e = compute_recv_layout(c, a.hidden, a.num_topk, &P.lay)) return e;
+    P.epoch[i] = ++c->comb_epoch;
+    c->comb_cum += (uint32_t)nb;
+    P.expected[i] = c->comb_cum;
+    P.rv[i] = c->view();
+    P.a[i] = a;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* kargs[] = {&P};
+  EPB_CUDA(cudaLaunchCooperativeKernel((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
+  return EPB_OK;
+}
+

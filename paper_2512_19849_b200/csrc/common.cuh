@@ -58,8 +58,16 @@ struct Scratch {                         // private to the owning rank
   uint64_t dst_rows[kMaxRanks];          // peer VA of dst's recv slot (this call)
   int32_t row_base[kMaxRanks];           // my first row inside dst's slot
   int32_t abort;                         // notify detected an error: skip data path
-  int32_t pad0;
+  uint32_t disp_arrive;                  // dispatch grid barrier: += 1 per block (monotonic)
+  uint32_t disp_go;                      // dispatch: epoch at which block 0 published the plan
+  uint32_t pad0;
+  int32_t ch_cnt[kMaxRanks][kMaxChannels];   // my tokens per (destination, channel), this call
+  int32_t ch_excl[kMaxRanks][kMaxChannels];  // exclusive prefix over channels of ch_cnt
   uint32_t ll_ticket[4];                 // LL last-warp tickets: [dispatch|combine][parity]
+  // LL epochs live on the device (bumped by each call's last warp) so LL calls
+  // can be captured in CUDA graphs and replayed: [dispatch|combine]
+  uint32_t ll_epoch[2];
+  uint32_t ll_pcnt[2];                   // proxy-transport calls so far (signal targets)
   // GPU -> CPU FIFOs: control arrays live in pinned host memory; the producer
   // keeps its tail (and a cached head) here, in device memory.
   uint64_t fifo_ctl[kMaxFifo];           // device aliases of the pinned ctl arrays
@@ -67,6 +75,9 @@ struct Scratch {                         // private to the owning rank
   int64_t fifo_head[kMaxFifo];
   int32_t fifo_channels;
   int32_t fifo_cap;
+  // phase timestamps (%globaltimer ns) written by block 0 / thread 0 when
+  // tracing is enabled (EPB_TRACE=1); read with epb_trace()
+  int64_t trace[64];
 };
 
 constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -90,6 +101,7 @@ struct RankView {
   char* peer[kMaxRanks];       // every rank's region, mapped in this process
   HostInfo* host;              // device alias of the pinned HostInfo
   uint64_t timeout_ns;
+  int trace;                   // record phase timestamps into Scratch::trace
 };
 
 __host__ __device__ inline Meta* meta_of(char* base) { return reinterpret_cast<Meta*>(base); }
@@ -128,10 +140,24 @@ __device__ __forceinline__ int64_t ld_volatile(const int64_t* p) {
   asm volatile("ld.volatile.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void fence_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
+// Release/acquire fence at system scope.  fence.sc is not needed anywhere on
+// this path (no store->load ordering across different flags is relied on) and
+// is far more expensive when many threads execute it.
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -165,6 +191,49 @@ __device__ __forceinline__ void st_na_v4(int4* p, const int4& v) {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Phase timestamp for tracing (first thread of the first block of the rank).
+__device__ __forceinline__ void trace_mark(const RankView& rv, int idx) {
+  if (rv.trace && threadIdx.x == 0 && blockIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    scratch_of(rv.base)->trace[idx] = (int64_t)t;
+  }
+}
+
+// gpu-scope acq_rel fetch-add (the last-arriver ticket pattern: each arriving
+// warp releases its prior stores, the winner acquires all of them and its own
+// sys-scope release then covers them by cumulativity).
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// In-place scan of n ints in shared memory by one warp (exclusive or
+// inclusive); returns the total.  Each lane owns a contiguous run of
+// ceil(n/32) elements, so the dependent chain is n/32 + 5 steps.
+__device__ __forceinline__ int warp_scan_smem(int32_t* a, int n, int lane, bool exclusive) {
+  const int per = (n + 31) / 32, base = lane * per;
+  int local = 0;
+  for (int i = 0; i < per; ++i)
+    if (base + i < n) local += a[base + i];
+  int incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  int run = incl - local;
+  for (int i = 0; i < per; ++i) {
+    if (base + i < n) {
+      const int v = a[base + i];
+      a[base + i] = exclusive ? run : run + v;
+      run += v;
+    }
+  }
+  return __shfl_sync(0xffffffffu, incl, 31);
+}
+
 // Record an error into the host-visible word (first error wins is not
 // required: any non-zero code makes the host raise).
 __device__ __forceinline__ void report_error(const RankView& rv, int code, int64_t detail) {
@@ -180,6 +249,22 @@ __device__ __forceinline__ bool wait_geq(const RankView& rv, const uint32_t* p, 
   uint64_t t0 = 0;
   int iter = 0;
   while (static_cast<int32_t>(ld_acquire_sys(p) - target) < 0) {
+    if ((++iter & 1023) == 0) {
+      uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > rv.timeout_ns) {
+        report_error(rv, EPB_ERR_DEADLOCK, tag);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+// Same, for a counter written only by this GPU (gpu-scope acquire).
+__device__ __forceinline__ bool wait_geq_gpu(const RankView& rv, const uint32_t* p, uint32_t target, int64_t tag) {
+  uint64_t t0 = 0;
+  int iter = 0;
+  while (static_cast<int32_t>(ld_acquire_gpu(p) - target) < 0) {
     if ((++iter & 1023) == 0) {
       uint64_t now = globaltimer();
       if (t0 == 0) t0 = now;

@@ -25,6 +25,7 @@ struct epb_ctx {
   uint64_t ll_proxy_disp = 0, ll_proxy_comb = 0;  // proxy-transport LL calls so far (signal targets)
   int num_sms = 148;
   uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;
+  int trace = 0;                        // EPB_TRACE=1: kernels record phase timestamps
   // LL bookkeeping of the last dispatch (shape) for combine validation.
   int ll_last_tokens = -1;
   // GPU -> CPU command FIFOs (pinned, mapped) and the proxy.
@@ -43,9 +44,14 @@ struct epb_ctx {
     for (int i = 0; i < epb::kMaxRanks; ++i) v.peer[i] = peer[i];
     v.host = host_dev;
     v.timeout_ns = timeout_ns;
+    v.trace = trace;
     return v;
   }
 };
+
+// normal-mode arena geometry and group validation (layout.cu)
+int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t* L);
+int check_group(epb_t* const* ctxs, int n);
 
 // error plumbing (api.cpp)
 int epb_set_error(int code, const std::string& msg);

@@ -1,0 +1,149 @@
+// layout.cu — the dispatch layout kernel (DeepEP get_dispatch_layout) and
+// the host-side geometry of the normal-mode receive arena.
+//
+// Layout = the reference's plan_dedup: a
+// token goes once to every distinct destination rank among its top-k
+// experts (on one NVLink node "node" == rank).  One thread per token;
+// histograms are warp-aggregated before touching shared memory:
+//   rank counts  : __ballot_sync per rank bit + popc (one smem add per warp)
+//   expert counts: __match_any_sync groups equal experts (one add per group)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+#include "ctx.h"
+
+namespace epb {
+
+constexpr int kLayoutThreads = 128;  // 4096 tokens -> 32 blocks
+
+__global__ void __launch_bounds__(kLayoutThreads) layout_kernel(const int64_t* __restrict__ topk_idx, int T, int k,
+                                                                 int E, int R, int32_t* __restrict__ per_rank,
+                                                                 int32_t* __restrict__ per_expert,
+                                                                 uint8_t* __restrict__ in_rank) {
+  extern __shared__ int64_t s_dyn[];
+  int64_t* s_topk = s_dyn;                                                   // [blockDim * k]
+  int32_t* s_hist = reinterpret_cast<int32_t*>(s_topk + (size_t)blockDim.x * k);  // [E + R]
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < E + R; i += blockDim.x) s_hist[i] = 0;
+  // stage this block's [tokens x k] tile with coalesced 16-byte loads
+  const int t_first = blockIdx.x * blockDim.x;
+  const int n_tok = min((int)blockDim.x, T - t_first);
+  const int n_words = n_tok * k;
+  const int64_t* src = topk_idx + (size_t)t_first * k;
+  if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (n_words % 2 == 0)) {
+    for (int i = tid; i < n_words / 2; i += blockDim.x)
+      reinterpret_cast<int4*>(s_topk)[i] = __ldg(reinterpret_cast<const int4*>(src) + i);
+  } else {
+    for (int i = tid; i < n_words; i += blockDim.x) s_topk[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  const int t = t_first + tid;
+  const int L = E / R;
+  uint32_t mask = 0;
+  const bool valid = t < T;
+  for (int j = 0; j < k; ++j) {
+    int64_t ej = valid ? s_topk[tid * k + j] : -1;
+    if (ej >= E) ej = -1;  // out-of-range experts are treated as masked
+    if (ej >= 0) mask |= 1u << (int)(ej / L);
+    const unsigned peers = __match_any_sync(0xffffffffu, (unsigned long long)ej);
+    if (ej >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[ej], __popc(peers));
+  }
+  if (valid) {
+    if (R == 8) {
+      uint64_t packed = 0;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) packed |= (uint64_t)((mask >> d) & 1u) << (8 * d);
+      *reinterpret_cast<uint64_t*>(in_rank + (size_t)t * 8) = packed;
+    } else {
+      for (int d = 0; d < R; ++d) in_rank[(size_t)t * R + d] = (mask >> d) & 1u;
+    }
+  }
+  for (int d = 0; d < R; ++d) {
+    const unsigned b = __ballot_sync(0xffffffffu, (mask >> d) & 1u);
+    if (lane == 0 && b) atomicAdd(&s_hist[E + d], __popc(b));
+  }
+  __syncthreads();
+  for (int i = tid; i < E; i += blockDim.x)
+    if (s_hist[i]) atomicAdd(&per_expert[i], s_hist[i]);
+  for (int i = tid; i < R; i += blockDim.x)
+    if (s_hist[E + i]) atomicAdd(&per_rank[i], s_hist[E + i]);
+}
+
+}  // namespace epb
+
+using namespace epb;
+
+// Geometry of the normal-mode arena for rows of `hidden` bf16 values and
+// `k` top-k entries: num_recv_slots receive slots + 2 (parity) combine
+// staging buffers, each holding cap_rows rows.  Identical on every rank.
+int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t* L) {
+  if (hidden <= 0 || hidden % 128 != 0) return epb_set_error(EPB_ERR_CONFIG, "hidden must be a positive multiple of 128");
+  if (k < 0 || k > 32) return epb_set_error(EPB_ERR_CONFIG, "num_topk must be in [0, 32]");
+  const size_t A = 256;
+  const size_t S = (size_t)hidden / 128;
+  const size_t x_row = 2 * (size_t)hidden;
+  const size_t per_row = x_row + S * 4 + (size_t)k * 12 + 4;
+  const size_t comb_row = 2 * (size_t)hidden + (size_t)k * 4;
+  const int ns = std::max(1, ctx->cfg.num_recv_slots);
+  const size_t overhead = A * (size_t)(6 * ns + 6);
+  if (ctx->cfg.nvl_bytes <= overhead) return epb_set_error(EPB_ERR_CONFIG, "num_nvl_bytes too small");
+  int64_t cap = (int64_t)((ctx->cfg.nvl_bytes - overhead) / (ns * per_row + 2 * comb_row));
+  cap &= ~(int64_t)15;
+  if (cap <= 0) return epb_set_error(EPB_ERR_CONFIG, "num_nvl_bytes too small for this hidden size");
+  std::memset(L, 0, sizeof(*L));
+  L->cap_rows = cap;
+  L->off_x = 0;
+  L->off_scales = align_up(cap * x_row, A);
+  L->off_topk_idx = align_up(L->off_scales + cap * S * 4, A);
+  L->off_topk_w = align_up(L->off_topk_idx + cap * (size_t)k * 8, A);
+  L->off_src_idx = align_up(L->off_topk_w + cap * (size_t)k * 4, A);
+  L->slot_bytes = align_up(L->off_src_idx + cap * 4, A);
+  L->slot0_off = ctx->arena_off();
+  const int64_t comb_bytes = align_up(cap * 2 * (size_t)hidden, A) + align_up(cap * (size_t)k * 4, A);
+  L->comb_w_off = align_up(cap * 2 * (size_t)hidden, A);
+  L->comb_off[0] = L->slot0_off + ns * L->slot_bytes;
+  L->comb_off[1] = L->comb_off[0] + comb_bytes;
+  if ((size_t)(L->comb_off[1] + comb_bytes - L->slot0_off) > ctx->cfg.nvl_bytes)
+    return epb_set_error(EPB_ERR_CONFIG, "internal: recv layout exceeds arena");
+  return EPB_OK;
+}
+
+int check_group(epb_t* const* ctxs, int n) {
+  if (!ctxs || n <= 0 || n > kMaxLocal) return epb_set_error(EPB_ERR_PROTOCOL, "bad local group");
+  for (int i = 0; i < n; ++i) {
+    if (!ctxs[i]) return epb_set_error(EPB_ERR_PROTOCOL, "null context");
+    for (int r = 0; r < ctxs[i]->world; ++r)
+      if (!ctxs[i]->peer[r]) return epb_set_error(EPB_ERR_CONNECTION, "peers not opened");
+  }
+  return EPB_OK;
+}
+
+extern "C" int epb_recv_layout(epb_t* ctx, int hidden, int num_topk, epb_recv_layout_t* out) {
+  if (!ctx || !out) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
+  return compute_recv_layout(ctx, hidden, num_topk, out);
+}
+
+extern "C" int epb_get_dispatch_layout(const int64_t* topk_idx, int num_tokens, int num_topk, int num_experts,
+                                       int num_ranks, int32_t* num_tokens_per_rank, int32_t* num_tokens_per_expert,
+                                       uint8_t* is_token_in_rank, void* stream) {
+  if (num_ranks <= 0 || num_ranks > kMaxRanks) return epb_set_error(EPB_ERR_CONFIG, "num_ranks out of range");
+  if (num_experts <= 0 || num_experts % num_ranks != 0)
+    return epb_set_error(EPB_ERR_CONFIG, "num_experts must be a positive multiple of num_ranks");
+  if (num_topk <= 0 || num_topk > 32) return epb_set_error(EPB_ERR_CONFIG, "num_topk must be in [1, 32]");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  EPB_CUDA(cudaMemsetAsync(num_tokens_per_rank, 0, sizeof(int32_t) * num_ranks, st));
+  EPB_CUDA(cudaMemsetAsync(num_tokens_per_expert, 0, sizeof(int32_t) * num_experts, st));
+  if (num_tokens == 0) return EPB_OK;
+  const int blocks = (num_tokens + kLayoutThreads - 1) / kLayoutThreads;
+  const size_t smem = sizeof(int64_t) * kLayoutThreads * num_topk + sizeof(int32_t) * (num_experts + num_ranks);
+  if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "num_experts too large for layout kernel");
+  if (smem > 48 * 1024)
+    EPB_CUDA(cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  layout_kernel<<<blocks, kLayoutThreads, smem, st>>>(topk_idx, num_tokens, num_topk, num_experts, num_ranks,
+                                                      num_tokens_per_rank, num_tokens_per_expert, is_token_in_rank);
+  EPB_CUDA(cudaGetLastError());
+  return EPB_OK;
+}

@@ -3,7 +3,7 @@ from __future__ import annotations
 
 import torch
 
-from ._lib import check, lib, ptr
+from ._lib import check, lib, ptr, raw_stream
 from .errors import ConfigError
 
 
@@ -17,7 +17,7 @@ def per_token_cast_to_fp8(x: torch.Tensor, round_scale: bool = False):
     q = torch.empty((T, H), dtype=torch.float8_e4m3fn, device=x.device)
     s = torch.empty((T, H // 128), dtype=torch.float32, device=x.device)
     check(lib.epb_per_token_cast_to_fp8(ptr(x), T, H, int(round_scale), ptr(q), ptr(s),
-                                        torch.cuda.current_stream().cuda_stream))
+                                        raw_stream()))
     return q, s
 
 
@@ -33,5 +33,5 @@ def get_dispatch_layout(topk_idx: torch.Tensor, num_experts: int, num_ranks: int
     per_expert = torch.empty(num_experts, dtype=torch.int32, device=dev)
     in_rank = torch.empty((T, num_ranks), dtype=torch.bool, device=dev)
     check(lib.epb_get_dispatch_layout(ptr(topk_idx), T, k, num_experts, num_ranks, ptr(per_rank), ptr(per_expert),
-                                      ptr(in_rank), torch.cuda.current_stream().cuda_stream))
+                                      ptr(in_rank), raw_stream()))
     return per_rank, per_expert, in_rank

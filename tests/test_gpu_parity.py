@@ -170,11 +170,11 @@ def test_recv_slot_leases_and_copy_out(torch):
     for r in held:
         for d in range(R):
             assert np.array_equal(bf16_bits(r[d][0]), out[d]["recv_x"])
-    assert all(len(rk._free) == 0 for rk in grp.ranks)
+    assert all(rk.num_free_slots() == 0 for rk in grp.ranks)
     del held, res, r2
     import gc
     gc.collect()
-    assert all(len(rk._free) == 1 for rk in grp.ranks)
+    assert all(rk.num_free_slots() == 1 for rk in grp.ranks)
     grp.destroy()
 
 
