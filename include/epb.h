@@ -145,6 +145,9 @@ typedef struct {
   const int32_t* rank_prefix_matrix;
   const uint8_t* is_token_in_rank;
   const int32_t* send_head;
+  const int32_t* channel_prefix_matrix;       /* [R, C] from the dispatch handle */
+  const int32_t* recv_channel_prefix_matrix;  /* [R, C] from the dispatch handle */
+  int num_channels;                           /* C of the dispatch (combine grid) */
   int num_tokens;
   void* combined_x;              /* [T, hidden] bf16                            */
   float* combined_topk_weights;  /* [T, num_topk] or NULL                       */

@@ -60,7 +60,9 @@ class DispatchArgs(C.Structure):
 
 class CombineArgs(C.Structure):
     _fields_ = [("x", vp), ("topk_weights", vp), ("num_recv", C.c_int), ("hidden", C.c_int), ("num_topk", C.c_int),
-                ("rank_prefix_matrix", vp), ("is_token_in_rank", vp), ("send_head", vp), ("num_tokens", C.c_int),
+                ("rank_prefix_matrix", vp), ("is_token_in_rank", vp), ("send_head", vp),
+                ("channel_prefix_matrix", vp), ("recv_channel_prefix_matrix", vp), ("num_channels", C.c_int),
+                ("num_tokens", C.c_int),
                 ("combined_x", vp), ("combined_topk_weights", vp)]
 
 

@@ -27,6 +27,16 @@ int epb_cuda_check(cudaError_t e, const char* what) {
 
 extern "C" const char* epb_last_error(void) { return g_last_error.c_str(); }
 
+cudaError_t epb_launch_grid_sync(const void* func, dim3 grid, dim3 block, void** args, size_t smem,
+                                 cudaStream_t st) {
+  static const bool coop = [] {
+    const char* s = std::getenv("EPB_COOP");
+    return !(s && s[0] == '0');
+  }();
+  if (coop) return cudaLaunchCooperativeKernel(func, grid, block, args, smem, st);
+  return cudaLaunchKernel(func, grid, block, args, smem, st);
+}
+
 extern "C" int epb_num_sms(void) {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;

@@ -256,7 +256,7 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* kargs[] = {&P};
-  EPB_CUDA(cudaLaunchCooperativeKernel((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
+  EPB_CUDA(epb_launch_grid_sync((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
   return EPB_OK;
 }
 

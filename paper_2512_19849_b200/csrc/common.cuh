@@ -51,6 +51,7 @@ struct Meta {
   uint32_t barrier[kMaxRanks];
   uint32_t pad[24];
   uint64_t proxy_sig[kMaxFifo][kMaxRanks];  // CPU-proxy signals: += 1 per piggybacked WRITE from src on channel
+  uint32_t comb_chunk[2][kMaxChannels];      // combine: rows landed per (parity, channel), all sources (monotonic)
   NotifyMsg mbox[2][kMaxRanks];
 };
 
@@ -61,6 +62,9 @@ struct Scratch {                         // private to the owning rank
   uint32_t disp_arrive;                  // dispatch grid barrier: += 1 per block (monotonic)
   uint32_t disp_go;                      // dispatch: epoch at which block 0 published the plan
   uint32_t pad0;
+  uint32_t comb_base[2][kMaxChannels];       // combine: comb_chunk value consumed by earlier calls
+  uint32_t comb_ticket[2];                   // combine: reduce work-queue head (per parity, reset by last warp)
+  uint32_t comb_finish[2];                   // combine: reducer warps done (per parity)
   int32_t ch_cnt[kMaxRanks][kMaxChannels];   // my tokens per (destination, channel), this call
   int32_t ch_excl[kMaxRanks][kMaxChannels];  // exclusive prefix over channels of ch_cnt
   uint32_t ll_ticket[4];                 // LL last-warp tickets: [dispatch|combine][parity]
@@ -245,10 +249,19 @@ __device__ __forceinline__ void report_error(const RankView& rv, int code, int64
 
 // Spin until *p >= target (wrap-safe for monotonically increasing u32
 // counters).  Returns false on timeout after reporting EPB_ERR_DEADLOCK.
-__device__ __forceinline__ bool wait_geq(const RankView& rv, const uint32_t* p, uint32_t target, int64_t tag) {
+// max_sleep_ns > 0: back off with __nanosleep (doubling from 32 ns) between
+// polls, for waits many warps run at once so polling does not steal L2 and
+// issue bandwidth from the warps doing the work.
+__device__ __forceinline__ bool wait_geq(const RankView& rv, const uint32_t* p, uint32_t target, int64_t tag,
+                                         unsigned max_sleep_ns = 0) {
   uint64_t t0 = 0;
   int iter = 0;
+  unsigned sleep_ns = 32;
   while (static_cast<int32_t>(ld_acquire_sys(p) - target) < 0) {
+    if (max_sleep_ns) {
+      __nanosleep(sleep_ns);
+      sleep_ns = min(sleep_ns * 2, max_sleep_ns);
+    }
     if ((++iter & 1023) == 0) {
       uint64_t now = globaltimer();
       if (t0 == 0) t0 = now;

@@ -49,6 +49,12 @@ struct epb_ctx {
   }
 };
 
+// Launch a kernel whose blocks wait on each other.  Default: a cooperative
+// launch (co-residency guaranteed by the driver).  EPB_COOP=0 switches to a
+// plain launch (grid is still sized to fit one wave); api.cpp.
+cudaError_t epb_launch_grid_sync(const void* func, dim3 grid, dim3 block, void** args, size_t smem,
+                                 cudaStream_t st);
+
 // normal-mode arena geometry and group validation (layout.cu)
 int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t* L);
 int check_group(epb_t* const* ctxs, int n);

@@ -356,7 +356,7 @@ extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* kargs[] = {&P};
-  EPB_CUDA(cudaLaunchCooperativeKernel((void*)dispatch_kernel, dim3(num_channels, n_local), dim3(kDispatchThreads),
+  EPB_CUDA(epb_launch_grid_sync((void*)dispatch_kernel, dim3(num_channels, n_local), dim3(kDispatchThreads),
                                        kargs, smem, st));
   return EPB_OK;
 }

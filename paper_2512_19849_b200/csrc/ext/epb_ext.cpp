@@ -305,8 +305,8 @@ py::list combine(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs,
   for (int i = 0; i < n; ++i) {
     Tensor x = xs[i].contiguous();
     TORCH_CHECK(x.scalar_type() == at::kBFloat16 && x.dim() == 2, "combine expects bf16 x [num_recv_tokens, hidden]");
-    Tensor rpm = hdls[i][0].cast<Tensor>(), recv_src = hdls[i][3].cast<Tensor>(), ir = hdls[i][4].cast<Tensor>(),
-           sh = hdls[i][5].cast<Tensor>();
+    Tensor rpm = hdls[i][0].cast<Tensor>(), cpm = hdls[i][1].cast<Tensor>(), rcpm = hdls[i][2].cast<Tensor>(),
+           recv_src = hdls[i][3].cast<Tensor>(), ir = hdls[i][4].cast<Tensor>(), sh = hdls[i][5].cast<Tensor>();
     const int N = (int)x.size(0), H = (int)x.size(1), T = (int)ir.size(0);
     if (N != recv_src.numel()) raise_code(EPB_ERR_PROTOCOL, "combine input rows do not match the dispatch handle");
     Tensor w;
@@ -327,6 +327,9 @@ py::list combine(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs,
     a.rank_prefix_matrix = rpm.data_ptr<int32_t>();
     a.is_token_in_rank = (const uint8_t*)ir.data_ptr();
     a.send_head = sh.data_ptr<int32_t>();
+    a.channel_prefix_matrix = cpm.data_ptr<int32_t>();
+    a.recv_channel_prefix_matrix = rcpm.data_ptr<int32_t>();
+    a.num_channels = (int)cpm.size(1);
     a.num_tokens = T;
     a.combined_x = o.data_ptr();
     a.combined_topk_weights = ow.defined() ? ow.data_ptr<float>() : nullptr;

@@ -6,10 +6,11 @@
 // experts (on one NVLink node "node" == rank).  One thread per token;
 // histograms are warp-aggregated before touching shared memory:
 //   rank counts  : __ballot_sync per rank bit + popc (one smem add per warp)
-//   expert counts: __match_any_sync groups equal experts (one add per group)
+//   expert counts: shared-memory atomics (random experts rarely collide)
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -17,7 +18,7 @@
 
 namespace epb {
 
-constexpr int kLayoutThreads = 128;  // 4096 tokens -> 32 blocks
+constexpr int kLayoutThreads = 512;  // 4096 tokens -> 8 blocks (8-way contention on the global histogram)
 
 __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(const int64_t* __restrict__ topk_idx, int T, int k,
                                                                  int E, int R, int32_t* __restrict__ per_rank,
@@ -45,11 +46,12 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(const int64_t* _
   uint32_t mask = 0;
   const bool valid = t < T;
   for (int j = 0; j < k; ++j) {
-    int64_t ej = valid ? s_topk[tid * k + j] : -1;
-    if (ej >= E) ej = -1;  // out-of-range experts are treated as masked
-    if (ej >= 0) mask |= 1u << (int)(ej / L);
-    const unsigned peers = __match_any_sync(0xffffffffu, (unsigned long long)ej);
-    if (ej >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[ej], __popc(peers));
+    const int64_t e64 = valid ? s_topk[tid * k + j] : -1;
+    const int e = (e64 >= 0 && e64 < E) ? (int)e64 : -1;  // out-of-range experts are treated as masked
+    if (e >= 0) {
+      mask |= 1u << (e / L);  // 32-bit division (the 64-bit one is a long software sequence)
+      atomicAdd(&s_hist[e], 1);
+    }
   }
   if (valid) {
     if (R == 8) {
@@ -134,15 +136,24 @@ extern "C" int epb_get_dispatch_layout(const int64_t* topk_idx, int num_tokens, 
     return epb_set_error(EPB_ERR_CONFIG, "num_experts must be a positive multiple of num_ranks");
   if (num_topk <= 0 || num_topk > 32) return epb_set_error(EPB_ERR_CONFIG, "num_topk must be in [1, 32]");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  EPB_CUDA(cudaMemsetAsync(num_tokens_per_rank, 0, sizeof(int32_t) * num_ranks, st));
-  EPB_CUDA(cudaMemsetAsync(num_tokens_per_expert, 0, sizeof(int32_t) * num_experts, st));
+  if (num_tokens_per_expert == num_tokens_per_rank + num_ranks) {  // contiguous counts: one memset
+    EPB_CUDA(cudaMemsetAsync(num_tokens_per_rank, 0, sizeof(int32_t) * (num_ranks + num_experts), st));
+  } else {
+    EPB_CUDA(cudaMemsetAsync(num_tokens_per_rank, 0, sizeof(int32_t) * num_ranks, st));
+    EPB_CUDA(cudaMemsetAsync(num_tokens_per_expert, 0, sizeof(int32_t) * num_experts, st));
+  }
   if (num_tokens == 0) return EPB_OK;
-  const int blocks = (num_tokens + kLayoutThreads - 1) / kLayoutThreads;
-  const size_t smem = sizeof(int64_t) * kLayoutThreads * num_topk + sizeof(int32_t) * (num_experts + num_ranks);
+  static const int threads = [] {
+    const char* s = std::getenv("EPB_LAYOUT_THREADS");
+    const int v = s ? std::atoi(s) : 128;
+    return (v >= 32 && v <= kLayoutThreads && v % 32 == 0) ? v : 128;
+  }();
+  const int blocks = (num_tokens + threads - 1) / threads;
+  const size_t smem = sizeof(int64_t) * threads * num_topk + sizeof(int32_t) * (num_experts + num_ranks);
   if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "num_experts too large for layout kernel");
   if (smem > 48 * 1024)
     EPB_CUDA(cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  layout_kernel<<<blocks, kLayoutThreads, smem, st>>>(topk_idx, num_tokens, num_topk, num_experts, num_ranks,
+  layout_kernel<<<blocks, threads, smem, st>>>(topk_idx, num_tokens, num_topk, num_experts, num_ranks,
                                                       num_tokens_per_rank, num_tokens_per_expert, is_token_in_rank);
   EPB_CUDA(cudaGetLastError());
   return EPB_OK;

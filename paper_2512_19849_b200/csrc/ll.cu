@@ -552,7 +552,7 @@ extern "C" int epb_ll_dispatch(epb_t* const* ctxs, int n_local, const epb_ll_dis
   const int nb = ll_blocks(ctxs, n_local, num_sms, (const void*)ll_dispatch_kernel, smem);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* kargs[] = {&P};
-  EPB_CUDA(cudaLaunchCooperativeKernel((void*)ll_dispatch_kernel, dim3(nb, n_local), dim3(kLLThreads), kargs, smem, st));
+  EPB_CUDA(epb_launch_grid_sync((void*)ll_dispatch_kernel, dim3(nb, n_local), dim3(kLLThreads), kargs, smem, st));
   return EPB_OK;
 }
 
@@ -579,7 +579,7 @@ extern "C" int epb_ll_combine(epb_t* const* ctxs, int n_local, const epb_ll_comb
   const int nb = ll_blocks(ctxs, n_local, num_sms, (const void*)ll_combine_kernel, 0);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* kargs[] = {&P};
-  EPB_CUDA(cudaLaunchCooperativeKernel((void*)ll_combine_kernel, dim3(nb, n_local), dim3(kLLThreads), kargs, 0, st));
+  EPB_CUDA(epb_launch_grid_sync((void*)ll_combine_kernel, dim3(nb, n_local), dim3(kLLThreads), kargs, 0, st));
   return EPB_OK;
 }
 
