@@ -84,6 +84,9 @@ __device__ __noinline__ void exchange_counts(const DispatchParams& P, int lr, in
   __shared__ int32_t s_tot[kMaxRanks];
   __shared__ int32_t s_rpm[kMaxRanks][kMaxRanks];
 
+  __shared__ int32_t s_exp[kMaxRanks * kMaxLocalExperts];  // num_tokens_per_expert, prefetched
+  const int E = a.num_tokens_per_expert != nullptr ? a.num_experts : 0;
+  for (int e = tid; e < E; e += nthr) s_exp[e] = __ldg(&a.num_tokens_per_expert[e]);  // overlaps the barrier
   if (tid == 0) wait_geq_gpu(rv, &sc->disp_arrive, P.target[lr], 0x180);
   __syncthreads();
   for (int i = tid; i < R * C; i += nthr) s_cnt[i / C][i % C] = __ldcg(&sc->ch_cnt[i / C][i % C]);
@@ -107,21 +110,8 @@ __device__ __noinline__ void exchange_counts(const DispatchParams& P, int lr, in
       msg->num_tokens = T;
     }
     for (int i = lane; i < C; i += 32) msg->channel_counts[i] = s_cnt[d][i];
-    if (a.num_tokens_per_expert != nullptr) {
-      for (int e0 = 0; e0 < L; e0 += 256) {  // 8 loads in flight per lane, then 8 stores
-        int v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int e = e0 + u * 32 + lane;
-          v[u] = e < L ? __ldg(&a.num_tokens_per_expert[d * L + e]) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int e = e0 + u * 32 + lane;
-          if (e < L) msg->expert_counts[e] = v[u];
-        }
-      }
-    }
+    if (a.num_tokens_per_expert != nullptr)
+      for (int e = lane; e < L; e += 32) msg->expert_counts[e] = s_exp[d * L + e];
     __syncwarp();
     if (lane == 0) st_release_sys(&meta_of(rv.peer[d])->mbox_flag[par][me], epoch);
   }
@@ -130,13 +120,11 @@ __device__ __noinline__ void exchange_counts(const DispatchParams& P, int lr, in
   __syncthreads();
   trace_mark(rv, 4);
 
-  // every source's counts -> prefix sums (staged in shared memory, warp scans)
-  for (int i = tid; i < R * C; i += nthr) s_cnt[i / C][i % C] = __ldcg(&my->mbox[par][i / C].channel_counts[i % C]);
+  // the rank prefix matrix first (all the plan needs); the per-channel receive
+  // prefix is a handle output and is computed after the plan is published
   if (tid < R * R) s_rpm[tid / R][tid % R] = __ldcg(&my->mbox[par][tid / R].counts_per_rank[tid % R]);
   __syncthreads();
-  if (warp < R) {
-    warp_scan_row(&s_cnt[warp][0], a.recv_channel_prefix_matrix + warp * C, nullptr, C, lane);
-  } else if (warp == R && lane < R) {
+  if (warp == 0 && lane < R) {
     const int d = lane;  // inclusive prefix over source rank, column d
     int run = 0;
     for (int s = 0; s < R; ++s) {
@@ -186,8 +174,25 @@ __device__ __noinline__ void exchange_counts(const DispatchParams& P, int lr, in
   __syncthreads();
   if (tid == 0) st_release_gpu(&sc->disp_go, epoch);  // the plan is visible to the other blocks
   trace_mark(rv, 5);
+}
 
-  // host publication: receive counts for the caller's tensor shapes
+// Block 0, warps [0, kPublishWarps): handle outputs and host publication,
+// while block 0's other warps already copy rows.
+constexpr int kPublishWarps = 2;
+__device__ __noinline__ void publish_counts(const DispatchParams& P, int lr, int C) {
+  const RankView& rv = P.rv[lr];
+  const epb_dispatch_args_t& a = P.a[lr];
+  const int R = rv.world, me = rv.rank;
+  const uint32_t epoch = P.epoch[lr];
+  const int par = epoch & 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int nthr = kPublishWarps * 32;
+  Meta* my = meta_of(rv.base);
+  // every source's per-channel counts -> receive channel prefix (handle output)
+  for (int d = warp; d < R; d += kPublishWarps)
+    warp_scan_row(&my->mbox[par][d].channel_counts[0], a.recv_channel_prefix_matrix + d * C, nullptr, C, lane);
+  // receive counts for the caller's tensor shapes
+  const int L = a.num_experts > 0 ? a.num_experts / R : 0;
   if (a.num_tokens_per_expert != nullptr) {
     const int align = max(1, a.expert_alignment);
     for (int le = tid; le < L; le += nthr) {
@@ -196,8 +201,8 @@ __device__ __noinline__ void exchange_counts(const DispatchParams& P, int lr, in
       rv.host->recv_per_expert[le] = (n + align - 1) / align * align;
     }
   }
-  if (tid == 0) rv.host->num_recv = s_rpm[R - 1][me];
-  __syncthreads();
+  if (tid == 0) rv.host->num_recv = a.rank_prefix_matrix[(R - 1) * R + me];
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   if (tid == 0) st_release_sys(const_cast<int64_t*>(&rv.host->notify_epoch), (int64_t)epoch);
   trace_mark(rv, 6);
 }
@@ -250,7 +255,9 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   __syncthreads();
   trace_mark(rv, 7);
 
-  // 3. push rows
+  // 3. push rows (block 0's first warps publish the counts meanwhile)
+  const int first_copy_warp = c == 0 ? kPublishWarps : 0;
+  if (warp < first_copy_warp) publish_counts(P, lr, C);
   if (!s_abort) {
     for (int i = tid; i < nt * R; i += blockDim.x) {  // handle: row of t inside my block at d, or -1
       const int p = s_pos[i];
@@ -260,7 +267,7 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     const int n16 = (int)(row_bytes >> 4);
     const int k = a.num_topk, S = a.num_scales;
     const int L = (a.topk_idx != nullptr && a.num_experts > 0) ? a.num_experts / R : 0;
-    for (int tt = warp; tt < nt; tt += nwarps) {
+    for (int tt = warp - first_copy_warp; tt >= 0 && tt < nt; tt += nwarps - first_copy_warp) {
       const int t = t0 + tt;
       const int4* src = reinterpret_cast<const int4*>(static_cast<const char*>(a.x) + (size_t)t * row_bytes);
       for (int base = 0; base < n16; base += 32 * kCopyUnroll) {

@@ -12,6 +12,9 @@
 
 namespace epb {
 
+// 8 warps per block.  (512-thread blocks fill the register file; the proxy
+// transport's same-device copies then could not make progress in the 1-GPU
+// emulated tests, so the LL grid leaves the SMs room to co-schedule them.)
 constexpr int kLLThreads = 256;
 constexpr float kFp8Max = 448.0f;
 
