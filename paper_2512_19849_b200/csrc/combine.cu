@@ -61,12 +61,14 @@ __device__ __forceinline__ int4 pack_bf16x8(const float* acc) {
 // loads in flight (U columns per lane per step, NV*U <= 8) so a warp has
 // >= 4 KB outstanding whatever the fan-in; accumulation is fp32 with one
 // rounding to bf16 at the end (canonical order).
+// Where rank d's partial of a token lives: base[d] + (row0[d] + send_head[t][d]) rows.
+//   push mode: base[me] = x (my input), base[d] = my staging (rows pushed back by d)
+//   pull mode: base[d] = d's input inside d's region, read over NVLink
 struct RowSrc {
-  const char* x;      // combine input (rows this rank received from itself)
-  const char* stage;  // staging (rows pushed back by peers)
+  const char* base[kMaxRanks];
+  const char* wbase[kMaxRanks];
+  int row0[kMaxRanks];
   size_t row_bytes;
-  int me, self_base;
-  int pre[kMaxRanks];
 };
 
 template <int NV>
@@ -77,9 +79,7 @@ __device__ __forceinline__ void reduce_rows(const RowSrc& rs, uint32_t mask, con
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int d = __fns(mask, 0, j + 1);  // (j+1)-th contributing rank, ascending
-    const int p = sh[d];
-    r[j] = reinterpret_cast<const int4*>(d == rs.me ? rs.x + (size_t)(rs.self_base + p) * rs.row_bytes
-                                                    : rs.stage + (size_t)(rs.pre[d] + p) * rs.row_bytes);
+    r[j] = reinterpret_cast<const int4*>(rs.base[d] + (size_t)(rs.row0[d] + sh[d]) * rs.row_bytes);
   }
   for (int base = lane; base < n16; base += 32 * U) {
     int4 v[U][NV];
@@ -145,11 +145,37 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   const bool abort = scratch_of(rv.base)->abort != 0;
   trace_mark(rv, 16);
 
-  // phase A: push rows back to their sources
+  // mode exchange: if every rank's combine input (and weights) lives inside its
+  // symmetric region — e.g. the zero-copy recv_x of the dispatch — tokens are
+  // reduced by reading the partials in place over NVLink (pull), with no push
+  // and no staging pass; otherwise rows are pushed back into staging first.
   const int N = a.num_recv;
+  __shared__ int64_t s_xoff[kMaxRanks], s_woff[kMaxRanks];
+  if (b == 0 && tid < R) {
+    const char* xp = static_cast<const char*>(a.x);
+    const char* wp = reinterpret_cast<const char*>(a.topk_weights);
+    const char* lo = rv.base;
+    const char* hi = rv.base + rv.region_bytes;
+    const bool xin = xp >= lo && xp + (size_t)N * row_bytes <= hi;
+    const bool win = wp == nullptr || (wp >= lo && wp + (size_t)N * k * 4 <= hi);
+    Meta* pm = meta_of(rv.peer[tid]);
+    pm->comb_msg[par][me].x_off = (xin && win) ? (int64_t)(xp - lo) : -1;
+    pm->comb_msg[par][me].w_off = (xin && win && wp != nullptr) ? (int64_t)(wp - lo) : -1;
+    st_release_sys(&pm->comb_mflag[par][me], epoch);
+  }
+  if (tid < R) {
+    wait_geq(rv, &meta_of(rv.base)->comb_mflag[par][tid], epoch, 0x380 + tid);
+    s_xoff[tid] = *reinterpret_cast<volatile int64_t*>(&meta_of(rv.base)->comb_msg[par][tid].x_off);
+    s_woff[tid] = *reinterpret_cast<volatile int64_t*>(&meta_of(rv.base)->comb_msg[par][tid].w_off);
+  }
+  __syncthreads();
+  bool pull = true;
+  for (int d = 0; d < R; ++d) pull = pull && s_xoff[d] >= 0;
+
+  // phase A (push mode): push rows back to their sources
   const int Jb = (N + nb - 1) / nb;
   const int j0 = b * Jb, j1 = min(N, j0 + Jb);
-  if (!abort) {
+  if (!abort && !pull) {
     for (int j = j0 + warp; j < j1; j += nwarps) {
       int s = 0;
       while (s < R - 1 && j >= s_excl[s] + s_cnt[s][me]) ++s;
@@ -177,8 +203,9 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   }
   __syncthreads();
   trace_mark(rv, 17);
+  // (pull mode still bumps the counters so the cumulative targets stay exact)
   if (tid < R) red_release_sys_add(&meta_of(rv.peer[tid])->comb_done[me], 1u);
-  if (tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
+  if (!pull && tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
   __syncthreads();
   trace_mark(rv, 18);
   if (abort) return;
@@ -189,13 +216,23 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   const int Tb = (T + nb - 1) / nb;
   const int tb0 = b * Tb, tb1 = min(T, tb0 + Tb);
   RowSrc rs;
-  rs.x = static_cast<const char*>(a.x);
-  rs.stage = my_stage;
   rs.row_bytes = row_bytes;
-  rs.me = me;
-  rs.self_base = s_excl[me];
 #pragma unroll
-  for (int d = 0; d < kMaxRanks; ++d) rs.pre[d] = s_mypre[d];
+  for (int d = 0; d < kMaxRanks; ++d) {
+    if (d == me) {
+      rs.base[d] = static_cast<const char*>(a.x);
+      rs.wbase[d] = reinterpret_cast<const char*>(a.topk_weights);
+      rs.row0[d] = s_excl[me];
+    } else if (pull) {
+      rs.base[d] = d < R ? rv.peer[d] + s_xoff[d] : nullptr;
+      rs.wbase[d] = (d < R && s_woff[d] >= 0) ? rv.peer[d] + s_woff[d] : nullptr;
+      rs.row0[d] = (d < R && me > 0) ? a.rank_prefix_matrix[(me - 1) * R + d] : 0;  // my first row at d
+    } else {
+      rs.base[d] = my_stage;
+      rs.wbase[d] = my_stage + P.lay.comb_w_off;
+      rs.row0[d] = s_mypre[d];
+    }
+  }
   for (int t = tb0 + warp; t < tb1; t += nwarps) {
     const int32_t* sh = a.send_head + (size_t)t * R;
     // contributing ranks as a bitmask; rows are taken in ascending rank order
@@ -219,10 +256,8 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
       float w = 0.0f;
       for (uint32_t m = mask; m != 0; m &= m - 1) {
         const int d = __ffs(m) - 1;
-        const int p = sh[d];
-        const float* wsrc = d == me ? a.topk_weights : reinterpret_cast<const float*>(my_stage + P.lay.comb_w_off);
-        const size_t widx = d == me ? (size_t)(rs.self_base + p) : (size_t)(rs.pre[d] + p);
-        if (wsrc != nullptr) w = __fadd_rn(w, wsrc[widx * k + lane]);
+        const float* wsrc = reinterpret_cast<const float*>(rs.wbase[d]);
+        if (wsrc != nullptr) w = __fadd_rn(w, wsrc[(size_t)(rs.row0[d] + sh[d]) * k + lane]);
       }
       a.combined_topk_weights[(size_t)t * k + lane] = w;
     }

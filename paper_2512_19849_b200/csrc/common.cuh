@@ -52,6 +52,10 @@ struct Meta {
   uint32_t pad[24];
   uint64_t proxy_sig[kMaxFifo][kMaxRanks];  // CPU-proxy signals: += 1 per piggybacked WRITE from src on channel
   uint32_t comb_chunk[2][kMaxChannels];      // combine: rows landed per (parity, channel), all sources (monotonic)
+  uint32_t comb_mflag[2][kMaxRanks];         // combine: epoch stamp of comb_msg[parity][src]
+  struct CombMsg {                           // combine: where src's input rows live (pull mode)
+    int64_t x_off, w_off;                    // offsets inside src's region (-1: not in the region)
+  } comb_msg[2][kMaxRanks];
   NotifyMsg mbox[2][kMaxRanks];
 };
 
@@ -106,6 +110,7 @@ struct RankView {
   HostInfo* host;              // device alias of the pinned HostInfo
   uint64_t timeout_ns;
   int trace;                   // record phase timestamps into Scratch::trace
+  uint64_t region_bytes;       // size of every rank's region
 };
 
 __host__ __device__ inline Meta* meta_of(char* base) { return reinterpret_cast<Meta*>(base); }

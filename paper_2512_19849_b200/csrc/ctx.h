@@ -45,6 +45,7 @@ struct epb_ctx {
     v.host = host_dev;
     v.timeout_ns = timeout_ns;
     v.trace = trace;
+    v.region_bytes = region_bytes;
     return v;
   }
 };
