@@ -37,6 +37,47 @@ cudaError_t epb_launch_grid_sync(const void* func, dim3 grid, dim3 block, void**
   return cudaLaunchKernel(func, grid, block, args, smem, st);
 }
 
+// Per-call launch-config queries are a few microseconds each; the dispatch and
+// combine calls sit on the host's critical path, so their answers are cached.
+namespace {
+std::mutex g_cfg_mu;
+struct OccKey {
+  const void* f;
+  int threads;
+  size_t smem;
+  int dev;
+};
+std::vector<std::pair<OccKey, int>> g_occ;
+std::vector<std::tuple<const void*, int, size_t>> g_smem;  // (func, device, granted max dynamic smem)
+}  // namespace
+
+int epb_max_active_blocks(const void* func, int threads, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(g_cfg_mu);
+  for (auto& kv : g_occ)
+    if (kv.first.f == func && kv.first.threads == threads && kv.first.smem == smem && kv.first.dev == dev)
+      return kv.second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, func, threads, smem) != cudaSuccess) n = 0;
+  g_occ.push_back({OccKey{func, threads, smem, dev}, n});
+  return n;
+}
+
+// Raises the kernel's dynamic shared-memory limit to `smem` (static shared
+// memory counts against the default 48 KB, so any nonzero request may need it).
+cudaError_t epb_ensure_smem(const void* func, size_t smem) {
+  if (smem == 0) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(g_cfg_mu);
+  for (auto& t : g_smem)
+    if (std::get<0>(t) == func && std::get<1>(t) == dev && std::get<2>(t) >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) g_smem.emplace_back(func, dev, smem);
+  return e;
+}
+
 extern "C" int epb_num_sms(void) {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;

@@ -276,8 +276,7 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
   std::memset(&P, 0, sizeof(P));
   P.n_local = n_local;
   int nb = std::max(1, num_sms / n_local);
-  int max_active = 0;
-  EPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_active, combine_kernel, kCombineThreads, 0));
+  const int max_active = epb_max_active_blocks((const void*)combine_kernel, kCombineThreads, 0);
   nb = std::min(nb, std::max(1, max_active * ctxs[0]->num_sms / n_local));
   for (int i = 0; i < n_local; ++i) {
     epb_ctx* c = ctxs[i];

@@ -56,6 +56,10 @@ struct epb_ctx {
 cudaError_t epb_launch_grid_sync(const void* func, dim3 grid, dim3 block, void** args, size_t smem,
                                  cudaStream_t st);
 
+// Cached launch-configuration queries (api.cpp).
+int epb_max_active_blocks(const void* func, int threads, size_t smem);
+cudaError_t epb_ensure_smem(const void* func, size_t smem);
+
 // normal-mode arena geometry and group validation (layout.cu)
 int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t* L);
 int check_group(epb_t* const* ctxs, int n);

@@ -347,10 +347,8 @@ extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_
   }
   const size_t smem = sizeof(int32_t) * (size_t)max_tc * ctxs[0]->world;
   if (smem > 160 * 1024) return epb_set_error(EPB_ERR_CONFIG, "too many tokens per channel; raise num_sms");
-  if (smem > 32 * 1024)
-    EPB_CUDA(cudaFuncSetAttribute(dispatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int max_active = 0;
-  EPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_active, dispatch_kernel, kDispatchThreads, smem));
+  EPB_CUDA(epb_ensure_smem((const void*)dispatch_kernel, smem));
+  const int max_active = epb_max_active_blocks((const void*)dispatch_kernel, kDispatchThreads, smem);
   if ((int64_t)num_channels * n_local > (int64_t)max_active * ctxs[0]->num_sms)
     return epb_set_error(EPB_ERR_CONFIG, "num_channels x ranks exceeds the co-resident grid; lower num_sms");
   for (int i = 0; i < n_local; ++i) {

@@ -151,8 +151,7 @@ extern "C" int epb_get_dispatch_layout(const int64_t* topk_idx, int num_tokens, 
   const int blocks = (num_tokens + threads - 1) / threads;
   const size_t smem = sizeof(int64_t) * threads * num_topk + sizeof(int32_t) * (num_experts + num_ranks);
   if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "num_experts too large for layout kernel");
-  if (smem > 48 * 1024)
-    EPB_CUDA(cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  EPB_CUDA(epb_ensure_smem((const void*)layout_kernel, smem));
   layout_kernel<<<blocks, threads, smem, st>>>(topk_idx, num_tokens, num_topk, num_experts, num_ranks,
                                                       num_tokens_per_rank, num_tokens_per_expert, is_token_in_rank);
   EPB_CUDA(cudaGetLastError());

@@ -503,10 +503,7 @@ static int check_group_ll(epb_t* const* ctxs, int n) {
 }
 
 static int ll_blocks(epb_t* const* ctxs, int n_local, int num_sms, const void* kernel, size_t smem) {
-  int max_active = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_active, kernel, kLLThreads, smem) != cudaSuccess ||
-      max_active < 1)
-    max_active = 1;
+  const int max_active = std::max(1, epb_max_active_blocks(kernel, kLLThreads, smem));
   int nb = std::max(1, num_sms / n_local);
   return std::min(nb, std::max(1, max_active * ctxs[0]->num_sms / n_local));
 }
@@ -547,8 +544,7 @@ extern "C" int epb_ll_dispatch(epb_t* const* ctxs, int n_local, const epb_ll_dis
   const size_t smem_recv = (size_t)(3 * P.g.R * P.g.L + P.g.L + 1) * 4;
   const size_t smem = std::max(smem_send, smem_recv);
   if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "LL dispatch shape needs too much shared memory");
-  if (smem > 48 * 1024)
-    EPB_CUDA(cudaFuncSetAttribute(ll_dispatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  EPB_CUDA(epb_ensure_smem((const void*)ll_dispatch_kernel, smem));
   const int nb = ll_blocks(ctxs, n_local, num_sms, (const void*)ll_dispatch_kernel, smem);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* kargs[] = {&P};
