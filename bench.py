@@ -350,6 +350,19 @@ def run_ours(args):
     e2e = {"value": round(job_bytes / (e2e_ms / 1e3) / 1e9, 4), "unit": "GB/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms / args.steps, 4)}
 
+    # ---- the other normal-mode rows of BASELINE.json (per-op device times) -------------------
+    configs = {}
+    if not args.no_configs:
+        common = (rank, R, dev, args, barrier, max_over_ranks, group)
+        for name, kw in (("dsv3_fp8_dispatch", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, fp8=True, buf=buf)),
+                         ("dsv3_bf16_combine_push", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, combine_in_region=False,
+                                                         buf=buf)),
+                         ("qwen3_235b_zipf", dict(T=8192, H=4096, E=128, zipf=1.0))):
+            try:
+                configs[name] = config_bench(name, *common, **kw)
+            except Exception as exc:
+                configs[name] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # ---- low-latency decode (128 tokens, FP8 dispatch + bf16 combine) ----------------------
     ll = {}
     for transport in (() if args.no_ll else ("nvlink", "proxy")):
@@ -370,7 +383,7 @@ def run_ours(args):
                            "experts": EXPERTS, "topk": TOPK, "parallelism": f"ep{R}",
                            "l2": f"{NSETS} rotating input sets ({NSETS * T_PER_RANK * ROW / 1e6:.0f} MB > 126 MB L2)"},
                 "per_gpu_gbs": round(value / R, 3),
-                "kernels_ms": kernels_ms, "roofline": roofline, "e2e": e2e, "ll_us": ll,
+                "kernels_ms": kernels_ms, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_scope": "per rank",
                 "clocks": clocks.summary(), "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
@@ -378,6 +391,75 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T, H, E, fp8=False, zipf=0.0,
+                 combine_in_region=True, buf=None):
+    """Per-op device times of the other BASELINE.json normal-mode rows
+    (SURVEY.md §8(d)): FP8 dispatch of DS-V3, Qwen3-235B with Zipf routing,
+    and combine on expert outputs allocated OUTSIDE the arena (push mode).
+    L2 is flushed (256 MB memset) before every op pair; the times are the
+    median over reps of the max over ranks, from CUDA events on the stream."""
+    import torch
+    import paper_2512_19849_b200 as epb
+    from tests.helpers import bf16_random, make_routing
+    own = buf is None
+    if own:
+        buf = epb.Buffer(group, epb.nvl_bytes_hint(T, H, R, TOPK, 2), 0, num_recv_slots=2)
+    g = np.random.default_rng(31_000 + 97 * rank + int(zipf * 10))
+    idx, w = make_routing(g, T, E, TOPK, zipf=zipf)
+    x = torch.from_numpy(bf16_random(g, (T, H)).view(np.int16)).view(torch.bfloat16).to(dev)
+    idx_t, w_t = torch.from_numpy(idx).to(dev), torch.from_numpy(w).to(dev)
+    x_in = epb.per_token_cast_to_fp8(x) if fp8 else x
+    row_bytes = (H + 4 * (H // 128)) if fp8 else 2 * H
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    m = torch.zeros(T, R, dtype=torch.bool, device=dev)
+    m.scatter_(1, idx_t // (E // R), True)
+    m[:, rank] = False
+    remote = int(m.sum())
+    reps = max(10, min(args.steps, 30))
+    d_ms, c_ms = [], []
+    for it in range(reps + 3):
+        per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(idx_t, E)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        barrier()
+        flush.zero_()  # also keeps the GPU busy while the host enqueues the op (device time only)
+        e[0].record()
+        recv_x, _, rtw, _, handle, _ = buf.dispatch(x_in, num_tokens_per_rank=per_rank, is_token_in_rank=in_rank,
+                                                    num_tokens_per_expert=per_exp, topk_idx=idx_t, topk_weights=w_t)
+        e[1].record()
+        if fp8 or not combine_in_region:  # expert outputs live in ordinary device memory
+            y = torch.empty((recv_x[0] if fp8 else recv_x).shape[0], H, dtype=torch.bfloat16, device=dev)
+            y.copy_(recv_x[0].to(torch.bfloat16) if fp8 else recv_x)
+        else:
+            y = recv_x
+        flush.zero_()
+        e[2].record()
+        buf.combine(y, handle, topk_weights=rtw)
+        e[3].record()
+        barrier()
+        if it >= 3:
+            d_ms.append(max_over_ranks(e[0].elapsed_time(e[1])))
+            c_ms.append(max_over_ranks(e[2].elapsed_time(e[3])))
+        del recv_x, y, handle
+    buf._g.check_device_error()
+    if own:
+        buf.destroy()
+    rem_max = max_over_ranks(float(remote))
+    d, c = statistics.median(d_ms), statistics.median(c_ms)
+    out = {"tokens_per_rank": T, "hidden": H, "experts": E, "topk": TOPK, "dispatch_dtype": "fp8" if fp8 else "bf16",
+           "routing": f"zipf({zipf})" if zipf else "uniform", "dispatch_us": round(d * 1e3, 2),
+           "combine_us": round(c * 1e3, 2), "combine_input": "arena view (pull)" if y_in_region(fp8, combine_in_region)
+           else "device tensor outside the arena (push)", "reps": reps}
+    if R > 1:
+        out["max_remote_rows"] = int(rem_max)
+        out["dispatch_nvlink_gbs"] = round(rem_max * row_bytes / (d / 1e3) / 1e9, 1)
+        out["combine_nvlink_gbs"] = round(rem_max * 2 * H / (c / 1e3) / 1e9, 1)
+    return out
+
+
+def y_in_region(fp8, combine_in_region):
+    return combine_in_region and not fp8
 
 
 def ll_bench(buf, transport, rank, R, dev, args, barrier, max_over_ranks):
@@ -461,6 +543,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ll", action="store_true", help="skip the low-latency sub-benchmarks (e.g. under ncu)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the FP8 / push-combine / Qwen3 sub-benchmarks")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

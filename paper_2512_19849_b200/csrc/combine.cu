@@ -64,12 +64,19 @@ __device__ __forceinline__ int4 pack_bf16x8(const float* acc) {
 // Where rank d's partial of a token lives: base[d] + (row0[d] + send_head[t][d]) rows.
 //   push mode: base[me] = x (my input), base[d] = my staging (rows pushed back by d)
 //   pull mode: base[d] = d's input inside d's region, read over NVLink
+// (kept in shared memory: it is indexed by the runtime rank id)
 struct RowSrc {
   const char* base[kMaxRanks];
   const char* wbase[kMaxRanks];
   int row0[kMaxRanks];
   size_t row_bytes;
 };
+
+// += 1 on destination d's per-source counter (gpu scope suffices for myself)
+__device__ __forceinline__ void bump_done(const RankView& rv, int d, int me) {
+  if (d == me) red_release_gpu_add(&meta_of(rv.peer[d])->comb_done[me], 1u);
+  else red_release_sys_add(&meta_of(rv.peer[d])->comb_done[me], 1u);
+}
 
 template <int NV>
 __device__ __forceinline__ void reduce_rows(const RowSrc& rs, uint32_t mask, const int32_t* sh, int4* out, int n16,
@@ -117,6 +124,7 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   const uint32_t epoch = P.epoch[lr];
   const int par = epoch & 1;
+  trace_mark(rv, 15);
   __shared__ int32_t s_cnt[kMaxRanks][kMaxRanks];  // count[s][d]
   __shared__ int32_t s_excl[kMaxRanks];            // first row from s in my receive order
   __shared__ int32_t s_sendpre[kMaxRanks];         // where my rows start in s's staging
@@ -151,22 +159,26 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   // and no staging pass; otherwise rows are pushed back into staging first.
   const int N = a.num_recv;
   __shared__ int64_t s_xoff[kMaxRanks], s_woff[kMaxRanks];
-  if (b == 0 && tid < R) {
+  if (b == 0 && tid < R) {  // my offsets to every peer: tagged words (16-byte / 4-byte units)
     const char* xp = static_cast<const char*>(a.x);
     const char* wp = reinterpret_cast<const char*>(a.topk_weights);
     const char* lo = rv.base;
     const char* hi = rv.base + rv.region_bytes;
-    const bool xin = xp >= lo && xp + (size_t)N * row_bytes <= hi;
-    const bool win = wp == nullptr || (wp >= lo && wp + (size_t)N * k * 4 <= hi);
-    Meta* pm = meta_of(rv.peer[tid]);
-    pm->comb_msg[par][me].x_off = (xin && win) ? (int64_t)(xp - lo) : -1;
-    pm->comb_msg[par][me].w_off = (xin && win && wp != nullptr) ? (int64_t)(wp - lo) : -1;
-    st_release_sys(&pm->comb_mflag[par][me], epoch);
+    const bool xin = xp >= lo && xp + (size_t)N * row_bytes <= hi && ((xp - lo) & 15) == 0 && (xp - lo) / 16 < kNotifyAbort;
+    const bool win = wp == nullptr || (wp >= lo && wp + (size_t)N * k * 4 <= hi && ((wp - lo) & 3) == 0 &&
+                                       (wp - lo) / 4 < kNotifyAbort);
+    const uint32_t xo = (xin && win) ? (uint32_t)((xp - lo) / 16) : kNotifyAbort;
+    const uint32_t wo = (xin && win && wp != nullptr) ? (uint32_t)((wp - lo) / 4) : kNotifyAbort;
+    uint64_t* m = meta_of(rv.peer[tid])->comb_msg[par][me];
+    st_relaxed_sys(&m[0], tagged(xo, epoch));
+    st_relaxed_sys(&m[1], tagged(wo, epoch));
   }
-  if (tid < R) {
-    wait_geq(rv, &meta_of(rv.base)->comb_mflag[par][tid], epoch, 0x380 + tid);
-    s_xoff[tid] = *reinterpret_cast<volatile int64_t*>(&meta_of(rv.base)->comb_msg[par][tid].x_off);
-    s_woff[tid] = *reinterpret_cast<volatile int64_t*>(&meta_of(rv.base)->comb_msg[par][tid].w_off);
+  if (tid < 2 * R) {
+    const int s = tid >> 1, f = tid & 1;
+    const uint32_t v = wait_tagged(rv, &meta_of(rv.base)->comb_msg[par][s][f], epoch, 0x380 + s);
+    const int64_t off = v == kNotifyAbort ? -1 : (int64_t)v * (f ? 4 : 16);
+    if (f) s_woff[s] = off;
+    else s_xoff[s] = off;
   }
   __syncthreads();
   bool pull = true;
@@ -203,11 +215,17 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   }
   __syncthreads();
   trace_mark(rv, 17);
-  // (pull mode still bumps the counters so the cumulative targets stay exact)
-  if (tid < R) red_release_sys_add(&meta_of(rv.peer[tid])->comb_done[me], 1u);
-  if (!pull && tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
-  __syncthreads();
+  // push mode: every source's rows have landed in my staging before I reduce.
+  // pull mode: the same counters are bumped after phase B instead, and mean
+  // "I have finished reading your input" — no rank returns (and lets its
+  // caller reuse the input) while a peer may still be reading it.
+  if (!pull || abort) {
+    if (tid < R) bump_done(rv, tid, me);
+    if (tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
+    __syncthreads();
+  }
   trace_mark(rv, 18);
+  trace_mark_max(rv, 21);
   if (abort) return;
 
   // phase B: reduce my tokens
@@ -215,10 +233,10 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   const int T = a.num_tokens;
   const int Tb = (T + nb - 1) / nb;
   const int tb0 = b * Tb, tb1 = min(T, tb0 + Tb);
-  RowSrc rs;
-  rs.row_bytes = row_bytes;
-#pragma unroll
-  for (int d = 0; d < kMaxRanks; ++d) {
+  __shared__ RowSrc rs;
+  if (tid == 0) rs.row_bytes = row_bytes;
+  if (tid < kMaxRanks) {
+    const int d = tid;
     if (d == me) {
       rs.base[d] = static_cast<const char*>(a.x);
       rs.wbase[d] = reinterpret_cast<const char*>(a.topk_weights);
@@ -233,6 +251,7 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
       rs.row0[d] = s_mypre[d];
     }
   }
+  __syncthreads();
   for (int t = tb0 + warp; t < tb1; t += nwarps) {
     const int32_t* sh = a.send_head + (size_t)t * R;
     // contributing ranks as a bitmask; rows are taken in ascending rank order
@@ -263,6 +282,12 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
     }
   }
   trace_mark(rv, 19);
+  trace_mark_max(rv, 20);
+  if (pull) {
+    __syncthreads();  // this block's reads of the peers' inputs are complete
+    if (tid < R) bump_done(rv, tid, me);
+    if (b == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
+  }
 }
 
 }  // namespace epb

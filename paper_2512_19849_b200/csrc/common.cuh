@@ -2,11 +2,14 @@
 //
 // Memory model used throughout ("release/acquire discipline"):
 //   * payload rows go to peer memory with plain 16-byte stores (NVLink posted
-//     writes), then every writer thread executes fence.sc.sys and the block
-//     barrier orders all of them before ONE st.release.sys / red.release.sys
-//     on the peer's flag/counter;
-//   * receivers spin with ld.acquire.sys on their own flag words, then a
-//     block barrier publishes the observation to the rest of the block.
+//     writes); a block barrier orders all of a block's stores before ONE
+//     red.release.sys on the destination's counter (release cumulativity);
+//   * receivers spin with ld.acquire.sys on their own counter words, then a
+//     block barrier publishes the observation to the rest of the block;
+//   * small control messages (dispatch counts, combine mode, host counts) are
+//     TAGGED words: value << 32 | call epoch, one naturally aligned 8-byte
+//     store each (single-copy atomic), so the data is its own flag — no
+//     fence on the writer, no flag round trip for the reader.
 // This replaces the reference ring's plain loads/stores (kernels.py:5-8,
 // kernels.py:67-79), which rely on x86-TSO and do not carry over to a
 // GPU <-> peer / GPU <-> host channel.
@@ -33,44 +36,39 @@ constexpr int kMaxFifo = 64;  // 6-bit channel_id (command.py:37)
 //   [kRegionHeader, +nvl_bytes)     normal-mode arena (recv slots + staging)
 //   [.., +ll_bytes)                 low-latency region
 // ---------------------------------------------------------------------------
-struct NotifyMsg {                       // one source rank's dispatch counts
-  int32_t counts_per_rank[kMaxRanks];    // src's num_tokens_per_rank
-  int32_t slot;                          // src's receive slot (where peers write TO src)
-  int32_t num_tokens;                    // src's T
-  int32_t pad[2];
-  int32_t channel_counts[kMaxChannels];  // src's tokens to me, per channel
-  int32_t expert_counts[kMaxLocalExperts];  // src's tokens for each of my local experts
+// Tagged word helpers: value << 32 | epoch (see the memory-model note).
+constexpr uint32_t kNotifyAbort = 0xffffffffu;  // "no value" (aborted call, not in region, ...)
+__host__ __device__ constexpr uint64_t tagged(uint32_t value, uint32_t epoch) {
+  return ((uint64_t)value << 32) | epoch;
+}
+
+struct NotifyMsg {                          // one source rank's dispatch counts (tagged words)
+  uint64_t counts_per_rank[kMaxRanks];      // src's num_tokens_per_rank
+  uint64_t slot;                            // src's receive slot (where peers write TO src)
+  uint64_t pad[7];
+  uint64_t channel_counts[kMaxChannels];    // src's tokens to me, per channel
+  uint64_t expert_counts[kMaxLocalExperts]; // src's tokens for each of my local experts
 };
 
 struct Meta {
-  uint32_t mbox_flag[2][kMaxRanks];      // epoch stamp of mbox[parity][src]
   uint32_t disp_done[kMaxRanks];         // += 1 per dispatch block of src (monotonic)
   uint32_t comb_done[kMaxRanks];         // += 1 per combine block of src (monotonic)
   uint64_t ll_disp_flag[2][kMaxRanks];   // LL dispatch: epoch stamp per src
   uint64_t ll_comb_flag[2][kMaxRanks];   // LL combine: epoch stamp per src
-  uint32_t barrier[kMaxRanks];
-  uint32_t pad[24];
   uint64_t proxy_sig[kMaxFifo][kMaxRanks];  // CPU-proxy signals: += 1 per piggybacked WRITE from src on channel
-  uint32_t comb_chunk[2][kMaxChannels];      // combine: rows landed per (parity, channel), all sources (monotonic)
-  uint32_t comb_mflag[2][kMaxRanks];         // combine: epoch stamp of comb_msg[parity][src]
-  struct CombMsg {                           // combine: where src's input rows live (pull mode)
-    int64_t x_off, w_off;                    // offsets inside src's region (-1: not in the region)
-  } comb_msg[2][kMaxRanks];
+  // combine mode message (tagged words): where src's input rows / weights live
+  // inside src's region, in 16-byte / 4-byte units (kNotifyAbort: not there)
+  uint64_t comb_msg[2][kMaxRanks][2];
   NotifyMsg mbox[2][kMaxRanks];
 };
 
 struct Scratch {                         // private to the owning rank
-  uint64_t dst_rows[kMaxRanks];          // peer VA of dst's recv slot (this call)
-  int32_t row_base[kMaxRanks];           // my first row inside dst's slot
-  int32_t abort;                         // notify detected an error: skip data path
-  uint32_t disp_arrive;                  // dispatch grid barrier: += 1 per block (monotonic)
-  uint32_t disp_go;                      // dispatch: epoch at which block 0 published the plan
-  uint32_t pad0;
-  uint32_t comb_base[2][kMaxChannels];       // combine: comb_chunk value consumed by earlier calls
-  uint32_t comb_ticket[2];                   // combine: reduce work-queue head (per parity, reset by last warp)
-  uint32_t comb_finish[2];                   // combine: reducer warps done (per parity)
-  int32_t ch_cnt[kMaxRanks][kMaxChannels];   // my tokens per (destination, channel), this call
-  int32_t ch_excl[kMaxRanks][kMaxChannels];  // exclusive prefix over channels of ch_cnt
+  int32_t abort;                         // the last dispatch aborted (combine skips its data path)
+  uint32_t pad0[3];
+  // dispatch, between the blocks of one rank (tagged words, this call's epoch):
+  uint64_t ch_cnt[kMaxRanks][kMaxChannels];   // my tokens per (destination, channel)
+  uint64_t ch_excl[kMaxRanks][kMaxChannels];  // exclusive prefix over channels of ch_cnt
+  uint64_t plan[2][kMaxRanks];                // [0][d]: d's receive slot (kNotifyAbort: aborted), [1][d]: my first row at d
   uint32_t ll_ticket[4];                 // LL last-warp tickets: [dispatch|combine][parity]
   // LL epochs live on the device (bumped by each call's last warp) so LL calls
   // can be captured in CUDA graphs and replayed: [dispatch|combine]
@@ -94,12 +92,15 @@ constexpr size_t kScratchBytes = align_up(sizeof(Scratch), 4096);
 constexpr size_t kRegionHeader = kMetaBytes + kScratchBytes;
 
 // Pinned, device-mapped host words the kernels publish to the CPU.
+// The dispatch publishes the receive counts to the host as tagged words, so
+// the host needs no flag and the kernel no system-scope fence (a fence.sys
+// would queue behind the copy warps' NVLink traffic on the SM).
+// notify[0] = number of received rows (kNotifyAbort if the call aborted),
+// notify[1 + e] = rows for local expert e (padded to expert_alignment).
 struct HostInfo {
-  volatile int64_t notify_epoch;
-  volatile int64_t num_recv;
   volatile int64_t err_code;
   volatile int64_t err_detail;
-  volatile int32_t recv_per_expert[kMaxLocalExperts];
+  volatile uint64_t notify[1 + kMaxLocalExperts];
 };
 
 // What a kernel needs to know about one (possibly emulated) rank.
@@ -128,6 +129,14 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
 }
 __device__ __forceinline__ void st_release_sys(int64_t* p, int64_t v) {
   asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(volatile uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const volatile uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
@@ -208,6 +217,14 @@ __device__ __forceinline__ void trace_mark(const RankView& rv, int idx) {
     scratch_of(rv.base)->trace[idx] = (int64_t)t;
   }
 }
+// Latest time any block reached this point (thread 0 of every block).
+__device__ __forceinline__ void trace_mark_max(const RankView& rv, int idx) {
+  if (rv.trace && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(reinterpret_cast<unsigned long long*>(&scratch_of(rv.base)->trace[idx]), (unsigned long long)t);
+  }
+}
 
 // gpu-scope acq_rel fetch-add (the last-arriver ticket pattern: each arriving
 // warp releases its prior stores, the winner acquires all of them and its own
@@ -278,7 +295,28 @@ __device__ __forceinline__ bool wait_geq(const RankView& rv, const uint32_t* p, 
   }
   return true;
 }
-// Same, for a counter written only by this GPU (gpu-scope acquire).
+// Spin until the tagged word *p carries `epoch`; returns its value, or
+// kNotifyAbort after reporting EPB_ERR_DEADLOCK on timeout.
+// sleep_ns > 0: __nanosleep between polls (for waits many blocks run at once).
+__device__ __forceinline__ uint32_t wait_tagged(const RankView& rv, const uint64_t* p, uint32_t epoch, int64_t tag,
+                                                unsigned sleep_ns = 0) {
+  uint64_t t0 = 0;
+  int iter = 0;
+  while (true) {
+    const uint64_t v = ld_relaxed_sys(p);
+    if ((uint32_t)v == epoch) return (uint32_t)(v >> 32);
+    if (sleep_ns) __nanosleep(sleep_ns);
+    if ((++iter & 1023) == 0) {
+      const uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > rv.timeout_ns) {
+        report_error(rv, EPB_ERR_DEADLOCK, tag);
+        return kNotifyAbort;
+      }
+    }
+  }
+}
+// Same as wait_geq, for a counter written only by this GPU (gpu-scope acquire).
 __device__ __forceinline__ bool wait_geq_gpu(const RankView& rv, const uint32_t* p, uint32_t target, int64_t tag) {
   uint64_t t0 = 0;
   int iter = 0;

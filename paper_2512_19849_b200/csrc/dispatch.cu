@@ -3,16 +3,18 @@
 //
 //   1. every block = one channel (a contiguous token range); warp d ballots
 //      the channel's tokens for destination d -> positions + per-channel count
-//   2. grid barrier; block 0 runs the count exchange ("notify"): channel
-//      prefix sums, one mailbox message per peer over NVLink (per-rank totals,
-//      per-channel counts, per-expert counts, my receive slot), waits for every
+//   2. block 0 runs the count exchange ("notify"): gathers every channel's
+//      counts, posts one mailbox message per peer over NVLink (per-rank totals,
+//      my receive slot, per-channel counts, per-expert counts), reads every
 //      peer's message, derives the rank prefix matrix and this rank's plan
-//      (destination slot address + first row per destination), publishes the
-//      plan with a gpu-scope release, then publishes the receive counts to the
-//      host (pinned memory) for the caller's tensor shapes
-//   3. all blocks read the plan and push every deduplicated row straight into
-//      its final row of the destination's receive slot: one HBM read per row,
-//      one 16-byte store per lane per destination (NVLink for peers)
+//      (destination slot + first row per destination); its first warps then
+//      publish the receive counts to the host (pinned memory) for the caller's
+//      tensor shapes.  Every control word on this path is a tagged word
+//      (common.cuh), so there is no grid barrier, no flag and no fence: each
+//      block polls exactly the words it needs.
+//   3. all blocks push every deduplicated row straight into its final row of
+//      the destination's receive slot: one HBM read per row, one 16-byte store
+//      per lane per destination (NVLink for peers)
 //   4. every block release-adds each destination's done counter; block 0 of
 //      every rank holds the kernel open until all sources have landed here.
 //
@@ -63,92 +65,216 @@ __device__ __forceinline__ int warp_scan_row(const int32_t* in, int32_t* incl_ou
 
 struct DispatchParams {
   int n_local, num_slots;
-  uint32_t epoch[kMaxLocal];   // per-call epoch: mailbox parity and the go flag value
-  uint32_t target[kMaxLocal];  // cumulative arrive / done target (sum of grid widths so far)
+  uint32_t epoch[kMaxLocal];   // per-call epoch: the tag of this call's mailbox / host words
+  uint32_t target[kMaxLocal];  // cumulative done target (sum of grid widths so far)
   RankView rv[kMaxLocal];
   epb_dispatch_args_t a[kMaxLocal];
   epb_recv_layout_t lay;
 };
 
-// Block 0's part: the cross-rank count exchange and the plan.
-__device__ __noinline__ void exchange_counts(const DispatchParams& P, int lr, int C) {
+// Block 0, warp R + d, at kernel start: my tokens for each of peer d's local
+// experts (known from the inputs alone, so they travel while the channels are
+// being counted; only the peer's host publication needs them).
+__device__ __forceinline__ void post_expert_counts(const DispatchParams& P, int lr, int d) {
   const RankView& rv = P.rv[lr];
   const epb_dispatch_args_t& a = P.a[lr];
-  const int R = rv.world, me = rv.rank, T = a.num_tokens;
+  const int R = rv.world, me = rv.rank, lane = threadIdx.x & 31;
+  const uint32_t epoch = P.epoch[lr];
+  NotifyMsg* msg = &meta_of(rv.peer[d])->mbox[epoch & 1][me];
+  const int L = a.num_experts > 0 ? a.num_experts / R : 0;
+  for (int base = 0; base < L; base += 32 * 8) {  // 8 loads in flight per lane, then the stores
+    int v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = base + j * 32 + lane;
+      v[j] = (e < L && a.num_tokens_per_expert != nullptr) ? __ldg(&a.num_tokens_per_expert[d * L + e]) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = base + j * 32 + lane;
+      if (e < L) st_relaxed_sys(&msg->expert_counts[e], tagged((uint32_t)v[j], epoch));
+    }
+  }
+}
+
+// Block 0, warps [0, kPublishWarps): the per-expert receive counts for the host
+// (tagged words, HostInfo), then the receive channel prefix (handle output), while
+// block 0's other warps already copy rows.  All of a thread's words are
+// loaded before any is checked (one round trip when they have all arrived).
+constexpr int kPublishWarps = 2;
+__device__ __forceinline__ void publish_counts(const DispatchParams& P, int lr, int C, bool aborted) {
+  const RankView& rv = P.rv[lr];
+  const epb_dispatch_args_t& a = P.a[lr];
+  const int R = rv.world;
+  const uint32_t epoch = P.epoch[lr];
+  const int par = epoch & 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int nthr = kPublishWarps * 32;
+  const Meta* my = meta_of(rv.base);
+  if (aborted) return;
+  const int L = a.num_experts > 0 ? a.num_experts / R : 0;
+  const int align = max(1, a.expert_alignment);
+  for (int le0 = tid; le0 < L; le0 += 2 * nthr) {
+    uint64_t v[2][kMaxRanks];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int s = 0; s < kMaxRanks; ++s) {
+        const int le = le0 + j * nthr;
+        v[j][s] = (s < R && le < L) ? ld_relaxed_sys(&my->mbox[par][s].expert_counts[le]) : tagged(0, epoch);
+      }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int le = le0 + j * nthr;
+      if (le >= L) break;
+      int n = 0;
+#pragma unroll
+      for (int s = 0; s < kMaxRanks; ++s)
+        if (s < R)
+          n += (uint32_t)v[j][s] == epoch ? (int)(v[j][s] >> 32)
+                                        : (int)wait_tagged(rv, &my->mbox[par][s].expert_counts[le], epoch, 0x140 + s);
+      n = (n + align - 1) / align * align;
+      st_relaxed_sys(&rv.host->notify[1 + le], tagged((uint32_t)n, epoch));
+    }
+  }
+  // every source's per-channel counts -> receive channel prefix (handle output)
+  constexpr int kChunks = kMaxChannels / 32;
+  for (int s = warp; s < R; s += kPublishWarps) {
+    uint64_t v[kChunks];
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      const int cc = q * 32 + lane;
+      v[q] = cc < C ? ld_relaxed_sys(&my->mbox[par][s].channel_counts[cc]) : tagged(0, epoch);
+    }
+    int run = 0;
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      if (q * 32 >= C) break;
+      const int cc = q * 32 + lane;
+      const int x = (uint32_t)v[q] == epoch ? (int)(v[q] >> 32)
+                                            : (int)wait_tagged(rv, &my->mbox[par][s].channel_counts[cc], epoch, 0x160 + s);
+      int incl = x;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += u;
+      }
+      if (cc < C) a.recv_channel_prefix_matrix[s * C + cc] = run + incl;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  trace_mark(rv, 6);
+}
+
+// Block 0: gather every channel's counts (tagged words), post my counts to the
+// peers, read theirs, and publish the plan (tagged words) for the other
+// blocks.  After the gather only warp 0 is on the critical path (peer
+// messages -> plan); the other warps publish the per-channel words meanwhile.
+__device__ __forceinline__ void exchange_counts(const DispatchParams& P, int lr, int C, int32_t (*s_cnt)[kMaxChannels],
+                                             int32_t (*s_rpm)[kMaxRanks], int32_t* s_slot, int* s_abort) {
+  const RankView& rv = P.rv[lr];
+  const epb_dispatch_args_t& a = P.a[lr];
+  const int R = rv.world, me = rv.rank;
   const uint32_t epoch = P.epoch[lr];
   const int par = epoch & 1;
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
   Scratch* sc = scratch_of(rv.base);
-  Meta* my = meta_of(rv.base);
-  __shared__ int32_t s_cnt[kMaxRanks][kMaxChannels];
-  __shared__ int32_t s_tot[kMaxRanks];
-  __shared__ int32_t s_rpm[kMaxRanks][kMaxRanks];
-
-  __shared__ int32_t s_exp[kMaxRanks * kMaxLocalExperts];  // num_tokens_per_expert, prefetched
-  const int E = a.num_tokens_per_expert != nullptr ? a.num_experts : 0;
-  for (int e = tid; e < E; e += nthr) s_exp[e] = __ldg(&a.num_tokens_per_expert[e]);  // overlaps the barrier
-  if (tid == 0) wait_geq_gpu(rv, &sc->disp_arrive, P.target[lr], 0x180);
-  __syncthreads();
-  for (int i = tid; i < R * C; i += nthr) s_cnt[i / C][i % C] = __ldcg(&sc->ch_cnt[i / C][i % C]);
+  const Meta* my = meta_of(rv.base);
+  trace_mark(rv, 2);
+  {
+    constexpr int kPer = kMaxRanks * kMaxChannels / kDispatchThreads;
+    uint64_t v[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + j * nthr;
+      v[j] = i < R * C ? ld_relaxed_sys(&sc->ch_cnt[i / C][i % C]) : tagged(0, epoch);
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + j * nthr;
+      if (i < R * C) {
+        const uint32_t x = (uint32_t)v[j] == epoch ? (uint32_t)(v[j] >> 32)
+                                                   : wait_tagged(rv, &sc->ch_cnt[i / C][i % C], epoch, 0x180);
+        if (x == kNotifyAbort) *s_abort = EPB_ERR_DEADLOCK;
+        s_cnt[i / C][i % C] = (int)x;
+      }
+    }
+  }
   __syncthreads();
   trace_mark(rv, 1);
   if (warp < R) {
-    const int tot = warp_scan_row(&s_cnt[warp][0], a.channel_prefix_matrix + warp * C, &sc->ch_excl[warp][0], C, lane);
-    if (lane == 0) s_tot[warp] = tot;
-  }
-  __syncthreads();
-  trace_mark(rv, 2);
-
-  // post my counts into every peer's mailbox (warp d -> peer d), then stamp the epoch
-  const int L = a.num_experts > 0 ? a.num_experts / R : 0;
-  if (warp < R) {
+    // what peer d's plan needs: my per-rank totals and my receive slot
     const int d = warp;
     NotifyMsg* msg = &meta_of(rv.peer[d])->mbox[par][me];
-    for (int i = lane; i < R; i += 32) msg->counts_per_rank[i] = s_tot[i];
-    if (lane == 0) {
-      msg->slot = a.recv_slot;
-      msg->num_tokens = T;
+    for (int i = 0; i < R; ++i) {
+      int s = 0;
+      for (int cc = lane; cc < C; cc += 32) s += s_cnt[i][cc];
+      s = __reduce_add_sync(0xffffffffu, s);
+      if (lane == i) st_relaxed_sys(&msg->counts_per_rank[i], tagged((uint32_t)s, epoch));
     }
-    for (int i = lane; i < C; i += 32) msg->channel_counts[i] = s_cnt[d][i];
-    if (a.num_tokens_per_expert != nullptr)
-      for (int e = lane; e < L; e += 32) msg->expert_counts[e] = s_exp[d * L + e];
-    __syncwarp();
-    if (lane == 0) st_release_sys(&meta_of(rv.peer[d])->mbox_flag[par][me], epoch);
+    if (lane == 31) st_relaxed_sys(&msg->slot, tagged((uint32_t)a.recv_slot, epoch));
+  } else if (warp < 2 * R) {
+    // each channel's offset inside my run to d (for my other blocks), the
+    // per-channel counts for peer d's handle, my channel prefix matrix row d
+    const int d = warp - R;
+    int run = 0;
+    for (int base = 0; base < C; base += 32) {
+      const int cc = base + lane;
+      const int v = cc < C ? s_cnt[d][cc] : 0;
+      int incl = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += u;
+      }
+      if (cc < C) st_relaxed_sys(&sc->ch_excl[d][cc], tagged((uint32_t)(run + incl - v), epoch));
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    NotifyMsg* msg = &meta_of(rv.peer[d])->mbox[par][me];
+    for (int cc = lane; cc < C; cc += 32)
+      st_relaxed_sys(&msg->channel_counts[cc], tagged((uint32_t)s_cnt[d][cc], epoch));
+    warp_scan_row(&s_cnt[d][0], a.channel_prefix_matrix + d * C, nullptr, C, lane);
   }
   trace_mark(rv, 3);
-  if (tid < R) wait_geq(rv, &my->mbox_flag[par][tid], epoch, 0x100 + tid);
-  __syncthreads();
-  trace_mark(rv, 4);
+  if (warp != 0) return;
 
-  // the rank prefix matrix first (all the plan needs); the per-channel receive
-  // prefix is a handle output and is computed after the plan is published
-  if (tid < R * R) s_rpm[tid / R][tid % R] = __ldcg(&my->mbox[par][tid / R].counts_per_rank[tid % R]);
-  __syncthreads();
-  if (warp == 0 && lane < R) {
-    const int d = lane;  // inclusive prefix over source rank, column d
-    int run = 0;
-    for (int s = 0; s < R; ++s) {
-      run += s_rpm[s][d];
-      s_rpm[s][d] = run;
-      a.rank_prefix_matrix[s * R + d] = run;
+  // warp 0: every source's totals and receive slot (<= 72 words, 3 per lane)
+  constexpr int kPer = (kMaxRanks * (kMaxRanks + 1) + 31) / 32;
+  uint64_t v[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int i = lane + 32 * j, s = i / (R + 1), f = i % (R + 1);
+    v[j] = i < R * (R + 1) ? ld_relaxed_sys(f < R ? &my->mbox[par][s].counts_per_rank[f] : &my->mbox[par][s].slot)
+                           : tagged(0, epoch);
+  }
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int i = lane + 32 * j, s = i / (R + 1), f = i % (R + 1);
+    if (i < R * (R + 1)) {
+      const uint64_t* w = f < R ? &my->mbox[par][s].counts_per_rank[f] : &my->mbox[par][s].slot;
+      const uint32_t x = (uint32_t)v[j] == epoch ? (uint32_t)(v[j] >> 32) : wait_tagged(rv, w, epoch, 0x100 + s);
+      if (x == kNotifyAbort) *s_abort = EPB_ERR_DEADLOCK;
+      if (f < R) s_rpm[s][f] = (int)x;
+      else s_slot[s] = (int)x;
     }
   }
-  __syncthreads();
-
-  // plan + capacity checks (every rank sees the same matrix, so all abort together)
-  if (tid < R) {
-    const int d = tid;
-    const int slot_d = __ldcg(&my->mbox[par][d].slot);
-    sc->dst_rows[d] = reinterpret_cast<uint64_t>(rv.peer[d] + P.lay.slot0_off + (int64_t)slot_d * P.lay.slot_bytes);
-    sc->row_base[d] = me > 0 ? s_rpm[me - 1][d] : 0;
+  __syncwarp();
+  trace_mark(rv, 4);
+  if (lane < R) {  // inclusive prefix over source rank, column d
+    int run = 0;
+    for (int s = 0; s < R; ++s) {
+      run += s_rpm[s][lane];
+      s_rpm[s][lane] = run;
+    }
   }
-  if (tid == 0) {
+  __syncwarp();
+  if (lane == 0 && *s_abort == 0) {
+    // capacity checks (every rank sees the same matrix, so all abort together)
     int err = 0;
     int64_t detail = 0;
     const int64_t cap = P.lay.cap_rows;
     for (int d = 0; d < R; ++d) {
-      const int slot_d = __ldcg(&my->mbox[par][d].slot);
-      if (slot_d < 0 || slot_d >= P.num_slots) {
+      if (s_slot[d] < 0 || s_slot[d] >= P.num_slots) {
         err = EPB_ERR_CONFIG;
         detail = 0x10000 + d;
       }
@@ -165,46 +291,25 @@ __device__ __noinline__ void exchange_counts(const DispatchParams& P, int lr, in
         detail = ((int64_t)sent << 8) | s;
       }
     }
-    sc->abort = err;
     if (err) {
+      *s_abort = err;
       rv.host->err_detail = detail;
       rv.host->err_code = err;
     }
   }
-  __syncthreads();
-  if (tid == 0) st_release_gpu(&sc->disp_go, epoch);  // the plan is visible to the other blocks
-  trace_mark(rv, 5);
-}
-
-// Block 0, warps [0, kPublishWarps): handle outputs and host publication,
-// while block 0's other warps already copy rows.
-constexpr int kPublishWarps = 2;
-__device__ __noinline__ void publish_counts(const DispatchParams& P, int lr, int C) {
-  const RankView& rv = P.rv[lr];
-  const epb_dispatch_args_t& a = P.a[lr];
-  const int R = rv.world, me = rv.rank;
-  const uint32_t epoch = P.epoch[lr];
-  const int par = epoch & 1;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int nthr = kPublishWarps * 32;
-  Meta* my = meta_of(rv.base);
-  // every source's per-channel counts -> receive channel prefix (handle output)
-  for (int d = warp; d < R; d += kPublishWarps)
-    warp_scan_row(&my->mbox[par][d].channel_counts[0], a.recv_channel_prefix_matrix + d * C, nullptr, C, lane);
-  // receive counts for the caller's tensor shapes
-  const int L = a.num_experts > 0 ? a.num_experts / R : 0;
-  if (a.num_tokens_per_expert != nullptr) {
-    const int align = max(1, a.expert_alignment);
-    for (int le = tid; le < L; le += nthr) {
-      int n = 0;
-      for (int s = 0; s < R; ++s) n += __ldcg(&my->mbox[par][s].expert_counts[le]);
-      rv.host->recv_per_expert[le] = (n + align - 1) / align * align;
-    }
+  __syncwarp();
+  const int ab = *s_abort;
+  if (lane < R) {
+    st_relaxed_sys(&sc->plan[0][lane], tagged(ab ? kNotifyAbort : (uint32_t)s_slot[lane], epoch));
+    st_relaxed_sys(&sc->plan[1][lane], tagged((uint32_t)(me > 0 ? s_rpm[me - 1][lane] : 0), epoch));
   }
-  if (tid == 0) rv.host->num_recv = a.rank_prefix_matrix[(R - 1) * R + me];
-  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
-  if (tid == 0) st_release_sys(const_cast<int64_t*>(&rv.host->notify_epoch), (int64_t)epoch);
-  trace_mark(rv, 6);
+  if (lane == 0) {
+    sc->abort = ab;
+    // the host sizes its receive tensors from this word (tagged, HostInfo)
+    st_relaxed_sys(&rv.host->notify[0], tagged(ab ? kNotifyAbort : (uint32_t)s_rpm[R - 1][me], epoch));
+  }
+  trace_mark(rv, 5);
+  for (int i = lane; i < R * R; i += 32) a.rank_prefix_matrix[i] = s_rpm[i / R][i % R];
 }
 
 __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __grid_constant__ DispatchParams P) {
@@ -213,13 +318,19 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   const epb_dispatch_args_t& a = P.a[lr];
   const int R = rv.world, me = rv.rank, C = gridDim.x, c = blockIdx.x, T = a.num_tokens;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const uint32_t epoch = P.epoch[lr];
   Scratch* sc = scratch_of(rv.base);
   extern __shared__ int32_t s_pos[];  // [Tc][R] row of the token inside its channel's run to d, or -1
+  __shared__ int32_t s_cnt[kMaxRanks][kMaxChannels];  // block 0: every channel's counts
+  __shared__ int32_t s_rpm[kMaxRanks][kMaxRanks];     // block 0: counts[src][dst], then prefix over src
+  __shared__ int32_t s_slot[kMaxRanks];
   __shared__ char* s_dst[kMaxRanks];
   __shared__ int32_t s_rb[kMaxRanks];
   __shared__ int32_t s_chx[kMaxRanks];
   __shared__ int s_abort;
   trace_mark(rv, 0);
+  if (tid == 0) s_abort = 0;
+  if (c == 0 && warp >= R && warp < 2 * R) post_expert_counts(P, lr, warp - R);
 
   // 1. channel-relative positions and per-(destination, channel) counts
   const int Tc = (T + C - 1) / C;
@@ -234,30 +345,40 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
       if (tt < nt) s_pos[tt * R + d] = in ? run + __popc(b & ((1u << lane) - 1)) : -1;
       run += __popc(b);
     }
-    if (lane == 0) sc->ch_cnt[d][c] = run;
+    if (lane == 0) st_relaxed_sys(&sc->ch_cnt[d][c], tagged((uint32_t)run, epoch));
   }
   __syncthreads();
-  if (tid == 0) red_release_gpu_add(&sc->disp_arrive, 1u);
 
-  // 2. block 0 exchanges counts with the peers and publishes the plan
+  // 2. block 0 exchanges counts with the peers and publishes the plan; the
+  //    other blocks read their part of it (tagged words, one warp polls)
   if (c == 0) {
-    exchange_counts(P, lr, C);
-  } else {
-    if (tid == 0) wait_geq_gpu(rv, &sc->disp_go, P.epoch[lr], 0x190);
+    exchange_counts(P, lr, C, s_cnt, s_rpm, s_slot, &s_abort);
     __syncthreads();
   }
-  if (tid < R) {
-    s_dst[tid] = reinterpret_cast<char*>(__ldcg(reinterpret_cast<const unsigned long long*>(&sc->dst_rows[tid])));
-    s_chx[tid] = __ldcg(&sc->ch_excl[tid][c]);          // this channel's offset inside my block at tid
-    s_rb[tid] = __ldcg(&sc->row_base[tid]) + s_chx[tid];  // first row of this channel's run at tid
+  if (warp == 0) {
+    for (int i = lane; i < 3 * R; i += 32) {
+      const int d = i % R, f = i / R;
+      const uint64_t* w = f == 0 ? &sc->plan[0][d] : f == 1 ? &sc->plan[1][d] : &sc->ch_excl[d][c];
+      const uint32_t v = wait_tagged(rv, w, epoch, 0x190, c == 0 ? 0 : 64);
+      if (f == 0) {
+        if (v == kNotifyAbort) s_abort = EPB_ERR_CONFIG;
+        else s_dst[d] = rv.peer[d] + P.lay.slot0_off + (int64_t)v * P.lay.slot_bytes;
+      } else if (f == 1) {
+        s_rb[d] = (int)v;
+      } else {
+        s_chx[d] = (int)v;
+      }
+    }
   }
-  if (tid == 0) s_abort = __ldcg(&sc->abort);
+  __syncthreads();
+  if (tid < R) s_rb[tid] += s_chx[tid];  // first row of this channel's run at tid
   __syncthreads();
   trace_mark(rv, 7);
+  trace_mark_max(rv, 11);
 
   // 3. push rows (block 0's first warps publish the counts meanwhile)
   const int first_copy_warp = c == 0 ? kPublishWarps : 0;
-  if (warp < first_copy_warp) publish_counts(P, lr, C);
+  if (warp < first_copy_warp) publish_counts(P, lr, C, s_abort != 0);
   if (!s_abort) {
     for (int i = tid; i < nt * R; i += blockDim.x) {  // handle: row of t inside my block at d, or -1
       const int p = s_pos[i];
@@ -316,7 +437,11 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   //    until every source's blocks have landed here
   __syncthreads();
   trace_mark(rv, 9);
-  if (tid < R) red_release_sys_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
+  trace_mark_max(rv, 12);
+  if (tid < R) {  // the local destination only needs gpu scope
+    if (tid == me) red_release_gpu_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
+    else red_release_sys_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
+  }
   if (c == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->disp_done[tid], P.target[lr], 0x200 + tid);
   trace_mark(rv, 10);
 }
@@ -369,11 +494,26 @@ extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_
 extern "C" int epb_wait_notify(epb_t* ctx, int64_t* num_recv, int32_t* num_recv_per_expert, int num_local_experts,
                                double timeout_s) {
   if (!ctx) return epb_set_error(EPB_ERR_PROTOCOL, "null context");
-  const int64_t want = ctx->disp_epoch;
+  if (num_recv_per_expert && (num_local_experts < 0 || num_local_experts > kMaxLocalExperts))
+    return epb_set_error(EPB_ERR_PROTOCOL, "num_local_experts out of range");
+  const uint32_t want = ctx->disp_epoch;
+  const int nwords = 1 + (num_recv_per_expert ? num_local_experts : 0);
+  volatile uint64_t* w = ctx->host->notify;
   auto t0 = std::chrono::steady_clock::now();
-  while (true) {
-    int64_t got = ctx->host->notify_epoch;
-    if (got == want) break;
+  int i = 0;
+  uint64_t v = 0;
+  while (i < nwords) {
+    v = w[i];
+    if ((uint32_t)v == want) {
+      if (i == 0) {
+        if ((uint32_t)(v >> 32) == kNotifyAbort) break;
+        if (num_recv) *num_recv = (int64_t)(v >> 32);
+      } else {
+        num_recv_per_expert[i - 1] = (int32_t)(v >> 32);
+      }
+      ++i;
+      continue;
+    }
     if (ctx->host->err_code != 0) break;
     if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
       cudaError_t ce = cudaGetLastError();
@@ -381,18 +521,15 @@ extern "C" int epb_wait_notify(epb_t* ctx, int64_t* num_recv, int32_t* num_recv_
       return epb_set_error(EPB_ERR_DEADLOCK, "dispatch timed out waiting for the peers' counts");
     }
   }
-  std::atomic_thread_fence(std::memory_order_acquire);
-  if (ctx->host->err_code != 0) {
+  if (i < nwords) {  // aborted: the error word is written (system scope) before the kernel returns
+    while (ctx->host->err_code == 0 &&
+           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() <= timeout_s) {
+    }
     char buf[160];
     snprintf(buf, sizeof(buf), "device reported error %lld (detail 0x%llx) in dispatch",
              (long long)ctx->host->err_code, (long long)ctx->host->err_detail);
-    return epb_set_error((int)ctx->host->err_code, buf);
-  }
-  if (num_recv) *num_recv = ctx->host->num_recv;
-  if (num_recv_per_expert) {
-    if (num_local_experts < 0 || num_local_experts > kMaxLocalExperts)
-      return epb_set_error(EPB_ERR_PROTOCOL, "num_local_experts out of range");
-    for (int i = 0; i < num_local_experts; ++i) num_recv_per_expert[i] = ctx->host->recv_per_expert[i];
+    const int code = ctx->host->err_code != 0 ? (int)ctx->host->err_code : EPB_ERR_DEADLOCK;
+    return epb_set_error(code, buf);
   }
   return EPB_OK;
 }
