@@ -272,6 +272,8 @@ class Buffer:
         if ll_transport == "proxy":
             self.start_proxy()
         self._g = _Group([self._rank])
+        self._native = self._rank.native
+        self._sms_key, self._sms_val = None, 0
         self._destroyed = False
 
     def start_proxy(self) -> None:
@@ -325,6 +327,15 @@ class Buffer:
     def _config(self, config):
         return config if config is not None else Config(Buffer.num_sms or None)
 
+    def _sms(self, config) -> int:
+        """SMs (= dispatch channels) for this call; one process per GPU."""
+        if config is not None:
+            return max(1, min(config.resolved_sms(), _device_sms()))
+        key = Buffer.num_sms
+        if self._sms_key != key:
+            self._sms_key, self._sms_val = key, max(1, min(Config(key or None).resolved_sms(), _device_sms()))
+        return self._sms_val
+
     # -- layout -----------------------------------------------------------------
     def get_dispatch_layout(self, topk_idx: torch.Tensor, num_experts: int,
                             previous_event: Optional[EventOverlap] = None, async_finish: bool = False,
@@ -343,22 +354,27 @@ class Buffer:
                  num_worst_tokens: int = 0, config: Optional[Config] = None,
                  previous_event: Optional[EventOverlap] = None, async_finish: bool = False,
                  allocate_on_comm_stream: bool = False):
-        _wait(previous_event)
-        recv_x, recv_topk_idx, recv_topk_w, per_expert_list, new_handle = self._g.dispatch(
-            [x], [handle], [is_token_in_rank], [num_tokens_per_expert], [topk_idx], [topk_weights],
-            expert_alignment, self._config(config))[0]
-        ev = _event(async_finish)
-        if handle is not None:
-            return recv_x, None, None, None, None, ev
-        return recv_x, recv_topk_idx, recv_topk_w, per_expert_list, new_handle, ev
+        if previous_event is not None:
+            previous_event.current_stream_wait()
+        xd, xs = (x[0], x[1]) if isinstance(x, tuple) else (x, None)
+        if handle is not None:  # cached layout: the handle carries is_token_in_rank
+            r = X.dispatch1(self._native, xd, xs, handle[4], None, None, None, expert_alignment, self._sms(config),
+                            self._g.timeout_s)
+            return r[0], None, None, None, None, _event(async_finish)
+        if is_token_in_rank is None:
+            raise ConfigError("is_token_in_rank is required without a handle")
+        r = X.dispatch1(self._native, xd, xs, is_token_in_rank, num_tokens_per_expert, topk_idx, topk_weights,
+                        expert_alignment, self._sms(config), self._g.timeout_s)
+        return r[0], r[1], r[2], r[3], r[4], _event(async_finish)
 
     def combine(self, x: torch.Tensor, handle: tuple, topk_weights: Optional[torch.Tensor] = None,
                 bias=None, config: Optional[Config] = None, previous_event: Optional[EventOverlap] = None,
                 async_finish: bool = False, allocate_on_comm_stream: bool = False):
         if bias is not None:
             raise UnsupportedOperation("combine bias is not supported")
-        _wait(previous_event)
-        out, out_w = self._g.combine([x], [handle], [topk_weights], self._config(config))[0]
+        if previous_event is not None:
+            previous_event.current_stream_wait()
+        out, out_w = X.combine1(self._native, x, handle, topk_weights, self._sms(config))
         return out, out_w, _event(async_finish)
 
     # -- low-latency mode -----------------------------------------------------------

@@ -12,6 +12,7 @@
 #include <ATen/cuda/CUDAContext.h>
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -90,6 +91,18 @@ struct Profiler {
 };
 Profiler g_prof;
 
+// Host-side phase timers of dispatch (microseconds, cumulative): prepare,
+// launch, wait for the counts, build the outputs.  Read with host_timers().
+struct HostTimers {
+  double t[4] = {0, 0, 0, 0};
+  long n = 0;
+};
+HostTimers g_ht;
+using Clock = std::chrono::steady_clock;
+inline double us_since(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double, std::micro>(b - a).count();
+}
+
 struct Rank {
   uintptr_t ctx = 0;
   int rank = 0, world = 1, num_slots = 1;
@@ -114,6 +127,14 @@ struct Rank {
   }
 };
 using RankP = std::shared_ptr<Rank>;
+
+// One leased receive slot; returned to its pool when the last view is freed.
+struct SlotLease {
+  std::shared_ptr<SlotPool> pool;
+  int slot;
+  SlotLease(std::shared_ptr<SlotPool> p, int s) : pool(std::move(p)), slot(s) {}
+  ~SlotLease() { pool->release(slot); }
+};
 
 std::vector<epb_t*> handles(const std::vector<RankP>& rs) {
   std::vector<epb_t*> v;
@@ -148,6 +169,7 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
                   const std::vector<c10::optional<Tensor>>& topk_idxs,
                   const std::vector<c10::optional<Tensor>>& topk_ws, int expert_alignment, int num_channels,
                   double timeout_s) {
+  const auto t0 = Clock::now();
   const int n = (int)ranks.size();
   const int R = ranks[0]->world, C = num_channels;
   std::vector<epb_dispatch_args_t> args(n);
@@ -223,9 +245,18 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
   {
     cudaEvent_t ev;
     g_prof.begin(&ev, stream);
+    const auto t1 = Clock::now();
     int rc = epb_dispatch(hs.data(), n, args.data(), C, stream);
+    const auto t2 = Clock::now();
     g_prof.end("dispatch", ev, stream);
+    g_ht.t[0] += us_since(t0, t1);
+    g_ht.t[1] += us_since(t1, t2);
     for (int i = 0; i < n && rc == 0; ++i) {
+      const auto tw0 = Clock::now();
+      struct Acc {
+        Clock::time_point a;
+        ~Acc() { g_ht.t[2] += us_since(a, Clock::now()); }
+      } acc{tw0};
       const int Lx = st[i].E ? st[i].E / R : 0;
       per_exp[i].resize(std::max(1, Lx));
       py::gil_scoped_release nogil;
@@ -238,6 +269,7 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
       raise_code(rc, msg);
     }
   }
+  const auto t3 = Clock::now();
   py::list out;
   for (int i = 0; i < n; ++i) {
     St& s = st[i];
@@ -245,53 +277,59 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
     const epb_recv_layout_t& L = *s.lay;
     const int64_t N = nrecv[i];
     char* slot_base = reinterpret_cast<char*>(rk.base + L.slot0_off + (int64_t)s.slot * L.slot_bytes);
+    const at::Device dev = s.x.device();
     auto opts = s.x.options();
-    Tensor mem;
-    if (s.copy_out) {
-      mem = at::from_blob(slot_base, {L.slot_bytes}, opts.dtype(at::kByte));
-    } else {
-      std::shared_ptr<SlotPool> pool = rk.pool;
-      const int slot = s.slot;
-      mem = at::from_blob(slot_base, {L.slot_bytes}, [pool, slot](void*) { pool->release(slot); },
-                          opts.dtype(at::kByte));
-    }
-    const int64_t rb = (int64_t)s.H * s.elem;
-    Tensor recv_x = mem.narrow(0, L.off_x, N * rb).view(s.elem == 2 ? at::kBFloat16 : at::kFloat8_e4m3fn)
-                        .view({N, s.H});
+    // zero-copy views of the leased slot: one tensor per output, all sharing
+    // the lease; the slot returns to the pool when the last of them is freed
+    std::shared_ptr<SlotLease> lease;
+    if (!s.copy_out) lease = std::make_shared<SlotLease>(rk.pool, s.slot);
+    auto view = [&](int64_t off, at::IntArrayRef sizes, at::ScalarType dt) -> Tensor {
+      void* p = slot_base + off;
+      if (s.copy_out) return at::for_blob(p, sizes).options(opts.dtype(dt)).target_device(dev).make_tensor().clone();
+      return at::for_blob(p, sizes)
+          .options(opts.dtype(dt))
+          .target_device(dev)
+          .deleter([lease](void*) {})
+          .make_tensor();
+    };
+    Tensor recv_x = view(L.off_x, {N, s.H}, s.elem == 2 ? at::kBFloat16 : at::kFloat8_e4m3fn);
     Tensor recv_scales, recv_ti, recv_tw;
-    if (s.xs.defined()) {
-      const int64_t S = s.xs.size(1);
-      recv_scales = mem.narrow(0, L.off_scales, N * S * 4).view(at::kFloat).view({N, S});
-    }
-    Tensor recv_src = mem.narrow(0, L.off_src_idx, N * 4).view(at::kInt);
+    if (s.xs.defined()) recv_scales = view(L.off_scales, {N, s.xs.size(1)}, at::kFloat);
+    Tensor recv_src = view(L.off_src_idx, {N}, at::kInt);
     if (s.ti.defined()) {
-      recv_ti = mem.narrow(0, L.off_topk_idx, N * s.k * 8).view(at::kLong).view({N, s.k});
-      if (s.tw.defined()) recv_tw = mem.narrow(0, L.off_topk_w, N * s.k * 4).view(at::kFloat).view({N, s.k});
+      recv_ti = view(L.off_topk_idx, {N, s.k}, at::kLong);
+      if (s.tw.defined()) recv_tw = view(L.off_topk_w, {N, s.k}, at::kFloat);
     }
-    if (s.copy_out) {
-      recv_x = recv_x.clone();
-      recv_src = recv_src.clone();
-      if (recv_scales.defined()) recv_scales = recv_scales.clone();
-      if (recv_ti.defined()) recv_ti = recv_ti.clone();
-      if (recv_tw.defined()) recv_tw = recv_tw.clone();
-    }
-    int32_t* hb = nullptr;
-    (void)hb;
-    Tensor rpm = s.hbuf.narrow(0, 0, (int64_t)R * R).view({R, R});
-    Tensor cpm = s.hbuf.narrow(0, (int64_t)R * R, (int64_t)R * C).view({R, C});
-    Tensor rcpm = s.hbuf.narrow(0, (int64_t)R * R + R * C, (int64_t)R * C).view({R, C});
-    Tensor send_head = s.hbuf.narrow(0, (int64_t)R * R + 2 * R * C, (int64_t)s.T * R).view({s.T, R});
+    // handle tensors: views of one int32 buffer
+    int32_t* hb = s.hbuf.data_ptr<int32_t>();
+    Tensor hkeep = s.hbuf;
+    auto hview = [&](int64_t off, at::IntArrayRef sizes) -> Tensor {
+      return at::for_blob(hb + off, sizes)
+          .options(opts.dtype(at::kInt))
+          .target_device(dev)
+          .deleter([hkeep](void*) {})
+          .make_tensor();
+    };
+    Tensor rpm = hview(0, {R, R});
+    Tensor cpm = hview((int64_t)R * R, {R, C});
+    Tensor rcpm = hview((int64_t)R * R + R * C, {R, C});
+    Tensor send_head = hview((int64_t)R * R + 2 * R * C, {s.T, R});
     py::object px = s.xs.defined() ? py::object(py::make_tuple(recv_x, recv_scales)) : py::cast(recv_x);
     py::object lst = py::none();
     if (s.E) {
-      py::list l;
-      for (int j = 0; j < s.E / R; ++j) l.append(per_exp[i][j]);
-      lst = l;
+      const int Lx = s.E / R;
+      PyObject* l = PyList_New(Lx);
+      if (!l) throw py::error_already_set();
+      for (int j = 0; j < Lx; ++j) PyList_SET_ITEM(l, j, PyLong_FromLong(per_exp[i][j]));
+      lst = py::reinterpret_steal<py::object>(l);
     }
     py::tuple handle = py::make_tuple(rpm, cpm, rcpm, recv_src, s.ir, send_head);
     out.append(py::make_tuple(px, recv_ti.defined() ? py::cast(recv_ti) : py::none(),
                               recv_tw.defined() ? py::cast(recv_tw) : py::none(), lst, handle));
   }
+  const auto t4 = Clock::now();
+  g_ht.t[3] += us_since(t3, t4);
+  g_ht.n += 1;
   return out;
 }
 
@@ -344,6 +382,22 @@ py::list combine(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs,
   check(epb_combine(hs.data(), n, args.data(), num_sms, stream));
   g_prof.end("combine", ev, stream);
   return out;
+}
+
+// Single-rank entry points (one process per GPU: the Buffer API), without the
+// per-call list packing of the group signatures.
+py::tuple dispatch1(const RankP& rank, const Tensor& x, const c10::optional<Tensor>& x_scales, const Tensor& in_rank,
+                    const c10::optional<Tensor>& per_expert, const c10::optional<Tensor>& topk_idx,
+                    const c10::optional<Tensor>& topk_w, int expert_alignment, int num_channels, double timeout_s) {
+  py::list r = dispatch({rank}, {x}, {x_scales}, {in_rank}, {per_expert}, {topk_idx}, {topk_w}, expert_alignment,
+                        num_channels, timeout_s);
+  return r[0].cast<py::tuple>();
+}
+
+py::tuple combine1(const RankP& rank, const Tensor& x, const py::tuple& handle, const c10::optional<Tensor>& topk_w,
+                   int num_sms) {
+  py::list r = combine({rank}, {x}, {handle}, {topk_w}, num_sms);
+  return r[0].cast<py::tuple>();
 }
 
 // ---------------------------------------------------------------------------
@@ -497,8 +551,21 @@ PYBIND11_MODULE(_epb_ext, m) {
   m.def("layout", &layout);
   m.def("dispatch", &dispatch);
   m.def("combine", &combine);
+  m.def("dispatch1", &dispatch1);
+  m.def("combine1", &combine1);
   m.def("ll_dispatch", &ll_dispatch);
   m.def("ll_combine", &ll_combine);
   m.def("set_profiling", [](bool on) { g_prof.on = on; });
+  m.def("host_timers", []() {
+    py::dict d;
+    const double n = g_ht.n ? (double)g_ht.n : 1.0;
+    d["calls"] = g_ht.n;
+    d["prepare_us"] = g_ht.t[0] / n;
+    d["launch_us"] = g_ht.t[1] / n;
+    d["wait_us"] = g_ht.t[2] / n;
+    d["outputs_us"] = g_ht.t[3] / n;
+    g_ht = HostTimers();
+    return d;
+  });
   m.def("collect_profile", []() { return g_prof.collect(); });
 }

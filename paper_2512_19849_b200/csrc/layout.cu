@@ -3,10 +3,14 @@
 //
 // Layout = the reference's plan_dedup: a
 // token goes once to every distinct destination rank among its top-k
-// experts (on one NVLink node "node" == rank).  One thread per token;
-// histograms are warp-aggregated before touching shared memory:
-//   rank counts  : __ballot_sync per rank bit + popc (one smem add per warp)
-//   expert counts: shared-memory atomics (random experts rarely collide)
+// experts (on one NVLink node "node" == rank).
+//
+// One cooperative kernel (no separate memset launch): block 0 zeroes the
+// count outputs while every block stages its [tokens x k] tile with 16-byte
+// loads and histograms it in shared memory (rank counts are warp-aggregated
+// with __ballot_sync + popc); a grid barrier then orders the zeroing before
+// the blocks' global atomics.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,56 +22,63 @@
 
 namespace epb {
 
-constexpr int kLayoutThreads = 512;  // 4096 tokens -> 8 blocks (8-way contention on the global histogram)
+constexpr int kLayoutThreads = 512;  // upper bound for EPB_LAYOUT_THREADS
 
 __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(const int64_t* __restrict__ topk_idx, int T, int k,
                                                                  int E, int R, int32_t* __restrict__ per_rank,
                                                                  int32_t* __restrict__ per_expert,
                                                                  uint8_t* __restrict__ in_rank) {
   extern __shared__ int64_t s_dyn[];
-  int64_t* s_topk = s_dyn;                                                   // [blockDim * k]
+  int64_t* s_topk = s_dyn;                                                        // [blockDim * k]
   int32_t* s_hist = reinterpret_cast<int32_t*>(s_topk + (size_t)blockDim.x * k);  // [E + R]
   const int tid = threadIdx.x, lane = tid & 31;
+  if (blockIdx.x == 0) {
+    for (int i = tid; i < E; i += blockDim.x) per_expert[i] = 0;
+    for (int i = tid; i < R; i += blockDim.x) per_rank[i] = 0;
+  }
   for (int i = tid; i < E + R; i += blockDim.x) s_hist[i] = 0;
-  // stage this block's [tokens x k] tile with coalesced 16-byte loads
-  const int t_first = blockIdx.x * blockDim.x;
-  const int n_tok = min((int)blockDim.x, T - t_first);
-  const int n_words = n_tok * k;
-  const int64_t* src = topk_idx + (size_t)t_first * k;
-  if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (n_words % 2 == 0)) {
-    for (int i = tid; i < n_words / 2; i += blockDim.x)
-      reinterpret_cast<int4*>(s_topk)[i] = __ldg(reinterpret_cast<const int4*>(src) + i);
-  } else {
-    for (int i = tid; i < n_words; i += blockDim.x) s_topk[i] = __ldg(src + i);
-  }
-  __syncthreads();
-  const int t = t_first + tid;
   const int L = E / R;
-  uint32_t mask = 0;
-  const bool valid = t < T;
-  for (int j = 0; j < k; ++j) {
-    const int64_t e64 = valid ? s_topk[tid * k + j] : -1;
-    const int e = (e64 >= 0 && e64 < E) ? (int)e64 : -1;  // out-of-range experts are treated as masked
-    if (e >= 0) {
-      mask |= 1u << (e / L);  // 32-bit division (the 64-bit one is a long software sequence)
-      atomicAdd(&s_hist[e], 1);
-    }
-  }
-  if (valid) {
-    if (R == 8) {
-      uint64_t packed = 0;
-#pragma unroll
-      for (int d = 0; d < 8; ++d) packed |= (uint64_t)((mask >> d) & 1u) << (8 * d);
-      *reinterpret_cast<uint64_t*>(in_rank + (size_t)t * 8) = packed;
+  for (int t_first = blockIdx.x * blockDim.x; t_first < T; t_first += gridDim.x * blockDim.x) {
+    // stage this tile with coalesced 16-byte loads
+    const int n_tok = min((int)blockDim.x, T - t_first);
+    const int n_words = n_tok * k;
+    const int64_t* src = topk_idx + (size_t)t_first * k;
+    __syncthreads();
+    if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (n_words % 2 == 0)) {
+      for (int i = tid; i < n_words / 2; i += blockDim.x)
+        reinterpret_cast<int4*>(s_topk)[i] = __ldg(reinterpret_cast<const int4*>(src) + i);
     } else {
-      for (int d = 0; d < R; ++d) in_rank[(size_t)t * R + d] = (mask >> d) & 1u;
+      for (int i = tid; i < n_words; i += blockDim.x) s_topk[i] = __ldg(src + i);
     }
-  }
-  for (int d = 0; d < R; ++d) {
-    const unsigned b = __ballot_sync(0xffffffffu, (mask >> d) & 1u);
-    if (lane == 0 && b) atomicAdd(&s_hist[E + d], __popc(b));
+    __syncthreads();
+    const int t = t_first + tid;
+    const bool valid = t < T;
+    uint32_t mask = 0;
+    for (int j = 0; j < k; ++j) {
+      const int64_t e64 = valid ? s_topk[tid * k + j] : -1;
+      const int e = (e64 >= 0 && e64 < E) ? (int)e64 : -1;  // out-of-range experts are treated as masked
+      if (e >= 0) {
+        mask |= 1u << (e / L);  // 32-bit division (the 64-bit one is a long software sequence)
+        atomicAdd(&s_hist[e], 1);
+      }
+    }
+    if (valid) {
+      if (R == 8) {
+        uint64_t packed = 0;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) packed |= (uint64_t)((mask >> d) & 1u) << (8 * d);
+        *reinterpret_cast<uint64_t*>(in_rank + (size_t)t * 8) = packed;
+      } else {
+        for (int d = 0; d < R; ++d) in_rank[(size_t)t * R + d] = (mask >> d) & 1u;
+      }
+    }
+    for (int d = 0; d < R; ++d) {
+      const unsigned b = __ballot_sync(0xffffffffu, (mask >> d) & 1u);
+      if (lane == 0 && b) atomicAdd(&s_hist[E + d], __popc(b));
+    }
   }
   __syncthreads();
+  cooperative_groups::this_grid().sync();  // block 0's zeroing is visible
   for (int i = tid; i < E; i += blockDim.x)
     if (s_hist[i]) atomicAdd(&per_expert[i], s_hist[i]);
   for (int i = tid; i < R; i += blockDim.x)
@@ -136,24 +147,27 @@ extern "C" int epb_get_dispatch_layout(const int64_t* topk_idx, int num_tokens, 
     return epb_set_error(EPB_ERR_CONFIG, "num_experts must be a positive multiple of num_ranks");
   if (num_topk <= 0 || num_topk > 32) return epb_set_error(EPB_ERR_CONFIG, "num_topk must be in [1, 32]");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (num_tokens_per_expert == num_tokens_per_rank + num_ranks) {  // contiguous counts: one memset
-    EPB_CUDA(cudaMemsetAsync(num_tokens_per_rank, 0, sizeof(int32_t) * (num_ranks + num_experts), st));
-  } else {
-    EPB_CUDA(cudaMemsetAsync(num_tokens_per_rank, 0, sizeof(int32_t) * num_ranks, st));
-    EPB_CUDA(cudaMemsetAsync(num_tokens_per_expert, 0, sizeof(int32_t) * num_experts, st));
-  }
-  if (num_tokens == 0) return EPB_OK;
   static const int threads = [] {
     const char* s = std::getenv("EPB_LAYOUT_THREADS");
     const int v = s ? std::atoi(s) : 128;
     return (v >= 32 && v <= kLayoutThreads && v % 32 == 0) ? v : 128;
   }();
-  const int blocks = (num_tokens + threads - 1) / threads;
   const size_t smem = sizeof(int64_t) * threads * num_topk + sizeof(int32_t) * (num_experts + num_ranks);
   if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "num_experts too large for layout kernel");
   EPB_CUDA(epb_ensure_smem((const void*)layout_kernel, smem));
-  layout_kernel<<<blocks, threads, smem, st>>>(topk_idx, num_tokens, num_topk, num_experts, num_ranks,
-                                                      num_tokens_per_rank, num_tokens_per_expert, is_token_in_rank);
+  const int per_sm = std::max(1, epb_max_active_blocks((const void*)layout_kernel, threads, smem));
+  int blocks = std::max(1, (num_tokens + threads - 1) / threads);
+  static int sms_cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& sms = sms_cache[dev & 63];
+  if (sms == 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  blocks = std::min(blocks, per_sm * std::max(1, sms));  // co-resident (grid-stride over token tiles)
+  const int64_t* ti = topk_idx;
+  int T = num_tokens, k = num_topk, E = num_experts, R = num_ranks;
+  void* kargs[] = {(void*)&ti, &T, &k, &E, &R, (void*)&num_tokens_per_rank, (void*)&num_tokens_per_expert,
+                   (void*)&is_token_in_rank};
+  EPB_CUDA(cudaLaunchCooperativeKernel((const void*)layout_kernel, dim3(blocks), dim3(threads), kargs, smem, st));
   EPB_CUDA(cudaGetLastError());
   return EPB_OK;
 }
