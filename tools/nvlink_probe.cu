@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include <vector>
+#include <chrono>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
 
@@ -136,6 +137,42 @@ int main(int argc, char** argv) {
     }
   }
   time([&] { CK(cudaMemcpyPeerAsync(d1, 1, d0, 0, bytes)); }, "ce cudaMemcpyPeerAsync");
+
+  // bidirectional: both GPUs move `bytes` to / from each other at once
+  // (what dispatch / combine do at EP=2); GB/s per direction
+  char *s1, *d1b;
+  CK(cudaSetDevice(1));
+  CK(cudaDeviceEnablePeerAccess(0, 0));
+  CK(cudaMalloc(&s1, bytes));
+  CK(cudaMalloc(&d1b, bytes));
+  CK(cudaMemset(s1, 2, bytes));
+  CK(cudaSetDevice(0));
+  auto bidir = [&](auto fn0, auto fn1, const char* name) {
+    for (int w = 0; w < 2; ++w) {
+      CK(cudaSetDevice(0)); fn0();
+      CK(cudaSetDevice(1)); fn1();
+    }
+    CK(cudaSetDevice(1)); CK(cudaDeviceSynchronize());
+    CK(cudaSetDevice(0)); CK(cudaDeviceSynchronize());
+    const int reps = 10;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; ++r) {
+      CK(cudaSetDevice(0)); fn0();
+      CK(cudaSetDevice(1)); fn1();
+    }
+    CK(cudaSetDevice(1)); CK(cudaDeviceSynchronize());
+    CK(cudaSetDevice(0)); CK(cudaDeviceSynchronize());
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    printf("%-40s %8.1f GB/s per direction\n", name, bytes * reps / s / 1e9);
+  };
+  bidir([&] { st_kernel<8><<<sms, 512>>>((int4*)d0, (int4*)d1b, n16); },
+        [&] { st_kernel<8><<<sms, 512>>>((int4*)s1, (int4*)d0b, n16); }, "bidir st U=8 148x512");
+  bidir([&] { st_kernel<8><<<sms * 2, 512>>>((int4*)s1, (int4*)d0b, n16); },
+        [&] { st_kernel<8><<<sms * 2, 512>>>((int4*)d0, (int4*)d1b, n16); }, "bidir ld U=8 296x512");
+  bidir([&] { st_kernel<16><<<sms * 2, 512>>>((int4*)s1, (int4*)d0b, n16); },
+        [&] { st_kernel<16><<<sms * 2, 512>>>((int4*)d0, (int4*)d1b, n16); }, "bidir ld U=16 296x512");
+  bidir([&] { CK(cudaMemcpyPeerAsync(d1b, 1, d0, 0, bytes)); },
+        [&] { CK(cudaMemcpyPeerAsync(d0b, 0, s1, 1, bytes)); }, "bidir ce");
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   printf("done\n");
