@@ -276,6 +276,21 @@ int epb_proxy_stats(epb_t* ctx, int64_t* out3);
  * "count only" mode.  elapsed_ns receives device time. */
 int epb_fifo_device_bench(epb_t* ctx, int64_t num_cmds, int channels, int64_t* elapsed_ns, void* stream);
 
+/* ---- Barrier TransferCmd ---------------
+ * The proxies' all-peer barrier: one shared-memory segment per job (ranks of one
+ * node), an epoch flag per rank.  Replaces the reference's barrier protocol
+ * (epsim models it in its transport simulator only).
+ * epb_barrier_*: the host rendezvous itself (also usable without a GPU).
+ * epb_proxy_barrier: stream-ordered GPU-side barrier: a kernel pushes a BARRIER
+ * command on `channel` and spins on check_completion of its index; the proxy
+ * completes it once every rank's proxy has entered (same_rail != 0: SameRail
+ * scope, which has no peers on one node and completes at once). */
+typedef struct epb_barrier epb_barrier_t;
+int epb_barrier_open(const char* name, int world, int rank, epb_barrier_t** out);
+int epb_barrier_wait(epb_barrier_t* b, int same_rail, double timeout_s);
+int epb_barrier_close(epb_barrier_t* b, int unlink_segment);
+int epb_proxy_barrier(epb_t* ctx, int channel, int same_rail, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

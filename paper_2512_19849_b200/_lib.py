@@ -137,6 +137,10 @@ _proto("epb_proxy_start", c_int, vp)
 _proto("epb_proxy_stop", c_int, vp)
 _proto("epb_proxy_stats", c_int, vp, P64)
 _proto("epb_fifo_device_bench", c_int, vp, i64, c_int, P64, vp)
+_proto("epb_barrier_open", c_int, C.c_char_p, c_int, c_int, C.POINTER(vp))
+_proto("epb_barrier_wait", c_int, vp, c_int, c_double)
+_proto("epb_barrier_close", c_int, vp, c_int)
+_proto("epb_proxy_barrier", c_int, vp, c_int, c_int, vp)
 
 # every symbol include/epb.h declares (checked by tests/test_abi.py)
 EXPORTED = [
@@ -147,7 +151,8 @@ EXPORTED = [
     "epb_cmd_unpack_fields", "epb_imm_encode_ll_batch", "epb_imm_encode_ht_batch", "epb_ring_push_batch",
     "epb_ring_pop_batch", "epb_ring_poll", "epb_ring_mark_completed", "epb_ring_check_completion",
     "epb_ring_shutdown", "epb_apply_deliveries", "epb_fifo_ctl", "epb_proxy_start", "epb_proxy_stop",
-    "epb_proxy_stats", "epb_fifo_device_bench",
+    "epb_proxy_stats", "epb_fifo_device_bench", "epb_barrier_open", "epb_barrier_wait", "epb_barrier_close",
+    "epb_proxy_barrier",
 ]
 
 

@@ -33,7 +33,7 @@ from typing import List, Optional, Sequence, Tuple, Union
 import torch
 
 from . import _lib as L
-from ._lib import check, lib
+from ._lib import check, lib, raw_stream
 from .errors import ConfigError, UnsupportedOperation, raise_for
 
 from . import _epb_ext as X  # noqa: E402  (needs libepb200.so loaded by _lib)
@@ -281,6 +281,14 @@ class Buffer:
         if not self._rank.proxy_running:
             check(lib.epb_proxy_start(self._rank.ctx))
             self._rank.proxy_running = True
+
+    def proxy_barrier(self, channel: int = 0, same_rail: bool = False) -> None:
+        """Stream-ordered all-peer barrier through the GPU->CPU FIFO: a kernel
+        pushes a Barrier TransferCmd on `channel` and waits on its completion,
+        which the proxy grants once every rank's proxy has entered
+        (PAPER.md:313-315, SPEC.md:274-282)."""
+        self.start_proxy()
+        check(lib.epb_proxy_barrier(self._rank.ctx, int(channel), int(bool(same_rail)), raw_stream()))
 
     # -- DeepEP helpers -------------------------------------------------------
     @staticmethod

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unistd.h>
 #include <string>
 
 #include "ctx.h"
@@ -140,6 +141,7 @@ extern "C" int epb_destroy(epb_t* ctx) {
   cudaDeviceSynchronize();
   epb_proxy_stop(ctx);
   epb_fifo_free(ctx);
+  if (ctx->barrier) epb_barrier_close(ctx->barrier, 1);
   for (int r = 0; r < ctx->world; ++r)
     if (ctx->peer_ipc[r] && ctx->peer[r]) cudaIpcCloseMemHandle(ctx->peer[r]);
   if (ctx->base) cudaFree(ctx->base);
@@ -172,6 +174,10 @@ extern "C" int epb_open_peers(epb_t* ctx, const void* handles) {
     ctx->peer[r] = static_cast<char*>(p);
     ctx->peer_ipc[r] = true;
   }
+  if (!ctx->barrier) {  // the proxies' all-peer barrier segment, named after the job's handles
+    const std::string name = epb_barrier_name(handles, (size_t)ctx->world * EPB_IPC_HANDLE_BYTES);
+    if (int rc = epb_barrier_open(name.c_str(), ctx->world, ctx->rank, &ctx->barrier)) return rc;
+  }
   return EPB_OK;
 }
 
@@ -183,6 +189,14 @@ extern "C" int epb_link_local(epb_t* const* ctxs, int n) {
   }
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) ctxs[i]->peer[j] = ctxs[j]->base;
+  const struct {
+    long pid;
+    const void* first;
+  } key{(long)getpid(), ctxs[0]};
+  const std::string name = epb_barrier_name(&key, sizeof(key));
+  for (int i = 0; i < n; ++i)
+    if (!ctxs[i]->barrier)
+      if (int rc = epb_barrier_open(name.c_str(), n, i, &ctxs[i]->barrier)) return rc;
   return EPB_OK;
 }
 

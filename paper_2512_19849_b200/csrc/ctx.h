@@ -32,6 +32,7 @@ struct epb_ctx {
   std::vector<int64_t*> fifo_host;      // ctl arrays (kernels.py:23-31 layout)
   std::vector<int64_t*> fifo_dev;       // device aliases
   epb_proxy* proxy = nullptr;
+  epb_barrier_t* barrier = nullptr;     // proxy all-peer barrier (barrier.cpp)
 
   size_t arena_off() const { return epb::kRegionHeader; }
   size_t ll_off() const { return epb::kRegionHeader + epb::align_up(cfg.nvl_bytes, 4096); }
@@ -59,6 +60,9 @@ cudaError_t epb_launch_grid_sync(const void* func, dim3 grid, dim3 block, void**
 // Cached launch-configuration queries (api.cpp).
 int epb_max_active_blocks(const void* func, int threads, size_t smem);
 cudaError_t epb_ensure_smem(const void* func, size_t smem);
+
+// name of the job-wide barrier segment (barrier.cpp)
+std::string epb_barrier_name(const void* bytes, size_t n);
 
 // normal-mode arena geometry and group validation (layout.cu)
 int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t* L);

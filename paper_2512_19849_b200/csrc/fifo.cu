@@ -60,9 +60,41 @@ __global__ void fifo_bench_kernel(RankView rv, int64_t n_per_ch, int channels, i
   }
 }
 
+// Barrier through the proxy (Barrier is blocking on the
+// GPU side): push one BARRIER command and spin on check_completion(idx).
+__global__ void proxy_barrier_kernel(RankView rv, int ch, int same_rail) {
+  if (threadIdx.x != 0) return;
+  uint64_t lo, hi;
+  cmd_pack_dev(EPB_CMD_BARRIER, (uint64_t)rv.rank, (uint64_t)ch, 0, 0, 0,
+               same_rail ? EPB_FLAG_SAME_RAIL_BARRIER : 0, lo, hi);
+  const int64_t idx = fifo_push(rv, ch, lo, hi);
+  if (idx < 0) return;
+  uint64_t t0 = 0;
+  int iter = 0;
+  while (!fifo_completed(rv, ch, idx)) {
+    if ((++iter & 255) == 0) {
+      const uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > rv.timeout_ns) {
+        report_error(rv, EPB_ERR_DEADLOCK, 0xa00 + ch);
+        return;
+      }
+    }
+  }
+}
+
 }  // namespace epb
 
 using namespace epb;
+
+extern "C" int epb_proxy_barrier(epb_t* ctx, int channel, int same_rail, void* stream) {
+  if (!ctx) return epb_set_error(EPB_ERR_PROTOCOL, "null context");
+  if (channel < 0 || channel >= ctx->cfg.fifo_channels) return epb_set_error(EPB_ERR_CONFIG, "no such FIFO channel");
+  if (!ctx->proxy) return epb_set_error(EPB_ERR_UNSUPPORTED, "proxy not running");
+  proxy_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(ctx->view(), channel, same_rail);
+  EPB_CUDA(cudaGetLastError());
+  return EPB_OK;
+}
 
 int epb_proxy_set_count_only(epb_ctx* ctx, bool on);  // proxy.cpp
 

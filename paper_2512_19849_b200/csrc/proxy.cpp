@@ -21,8 +21,9 @@
 //              after all earlier commands of the channel.  The peer counter has
 //              a single writer (this channel), so the add is a shadow-value store.
 //   DRAIN   -> waits for every copy issued on the channel.
-//   BARRIER -> UnsupportedOperation on a single NVLink node (rail barriers are
-//              an inter-node protocol).
+//   BARRIER -> drains the channel, then the all-peer rendezvous of barrier.cpp
+//              (SPEC.md:274-282); SameRail completes at once on one node.
+//              The thread blocks meanwhile ("Barrier and Drain are blocking").
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -147,6 +148,17 @@ void serve(epb_proxy* px, ChanState& cs, std::unordered_map<uint64_t, uint64_t>&
       flush(px, cs);
       cudaStreamSynchronize(cs.st);
       break;
+    case EPB_CMD_BARRIER: {
+      // everything this channel issued before the barrier has landed, then
+      // the all-peer rendezvous (barrier.cpp); COMPLETED advances after it
+      flush(px, cs);
+      cudaStreamSynchronize(cs.st);
+      const double timeout_s = (double)ctx->timeout_ns * 1e-9;
+      if (!ctx->barrier) proxy_error(ctx, EPB_ERR_CONNECTION, 0xba);
+      else if (epb_barrier_wait(ctx->barrier, (flags & EPB_FLAG_SAME_RAIL_BARRIER) != 0, timeout_s) != EPB_OK)
+        proxy_error(ctx, EPB_ERR_DEADLOCK, 0xbb);
+      break;
+    }
     default:
       flush(px, cs);
       proxy_error(ctx, EPB_ERR_UNSUPPORTED, kind);

@@ -97,6 +97,22 @@ def _worker(rank, world, port, results):
                 ref = O.ll_combine([[ys2[d][le, : o2[d][le]["count"]] for le in range(L)] for d in range(R)],
                                    idx2, w2, E2)
                 assert np.array_equal(bf16_bits(comb), ref[rank]), f"{transport} LL combine"
+            if transport == "proxy":
+                # Barrier TransferCmd: no rank's barrier completes before the last
+                # rank entered; ranks enter 0.25 s apart
+                import time
+                for rep in range(2):
+                    dist.barrier()
+                    time.sleep(0.25 * ((rank + rep) % R))
+                    t_in = time.time()
+                    b2.proxy_barrier(channel=rep)
+                    torch.cuda.synchronize()
+                    t_out = time.time()
+                    ts = [None] * R
+                    dist.all_gather_object(ts, (t_in, t_out))
+                    assert min(o for _, o in ts) >= max(i for i, _ in ts) - 0.002, f"proxy barrier released early {ts}"
+                b2.proxy_barrier(same_rail=True)  # no rail peers on one node: completes at once
+                torch.cuda.synchronize()
             b2.destroy()
         dist.barrier()
         dist.destroy_process_group()

@@ -171,6 +171,26 @@ int main(int argc, char** argv) {
         [&] { st_kernel<8><<<sms * 2, 512>>>((int4*)d0, (int4*)d1b, n16); }, "bidir ld U=8 296x512");
   bidir([&] { st_kernel<16><<<sms * 2, 512>>>((int4*)s1, (int4*)d0b, n16); },
         [&] { st_kernel<16><<<sms * 2, 512>>>((int4*)d0, (int4*)d1b, n16); }, "bidir ld U=16 296x512");
+  for (int ch : {4096, 8192, 16384}) {
+    auto k = ch == 4096 ? tma_kernel<4096> : ch == 8192 ? tma_kernel<8192> : tma_kernel<16384>;
+    for (int warps : {4, 8}) {
+      const size_t smem = (size_t)warps * 2 * ch;
+      if (smem > 200 * 1024) continue;
+      CK(cudaSetDevice(1));
+      CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(cudaSetDevice(0));
+      CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      char name[64];
+      snprintf(name, sizeof name, "tma pull chunk %d, %d warps/blk", ch, warps);
+      time([&] { k<<<sms, warps * 32, smem>>>(s1, d0b, bytes); }, name);
+      snprintf(name, sizeof name, "bidir tma pull chunk %d, %d warps/blk", ch, warps);
+      bidir([&] { k<<<sms, warps * 32, smem>>>(s1, d0b, bytes); },
+            [&] { k<<<sms, warps * 32, smem>>>(d0, d1b, bytes); }, name);
+      snprintf(name, sizeof name, "bidir tma push chunk %d, %d warps/blk", ch, warps);
+      bidir([&] { k<<<sms, warps * 32, smem>>>(d0, d1b, bytes); },
+            [&] { k<<<sms, warps * 32, smem>>>(s1, d0b, bytes); }, name);
+    }
+  }
   bidir([&] { CK(cudaMemcpyPeerAsync(d1b, 1, d0, 0, bytes)); },
         [&] { CK(cudaMemcpyPeerAsync(d0b, 0, s1, 1, bytes)); }, "bidir ce");
   CK(cudaGetLastError());
