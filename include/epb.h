@@ -67,6 +67,9 @@ typedef struct {
   int fifo_channels;    /* GPU->CPU command FIFOs (0 = no proxy)            */
   int fifo_capacity;    /* kMaxInflight per FIFO, power of two */
   int proxy_threads;    /* CPU proxy threads (PAPER.md:469 uses 4)          */
+  int ht_transport;     /* normal mode data path: 0 = NVLink stores from the
+                           kernels, 1 = CPU proxy (WRITE/ATOMIC TransferCmds;
+                           the arena then also holds one send-staging slot)  */
 } epb_config_t;
 
 int epb_create(epb_t** out, int rank, int world, const epb_config_t* cfg);
@@ -105,6 +108,7 @@ typedef struct {
   int64_t comb_off[2];     /* combine staging (parity) offsets in the region     */
   int64_t comb_w_off;      /* weights offset inside a combine staging buffer     */
   int64_t slot0_off;       /* offset of slot 0 in the region                     */
+  int64_t send_off;        /* proxy transport: send-staging slot offset (else 0) */
 } epb_recv_layout_t;
 
 int epb_recv_layout(epb_t* ctx, int hidden, int num_topk, epb_recv_layout_t* out);

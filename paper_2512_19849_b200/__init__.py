@@ -10,7 +10,16 @@ Public surface:
 Everything executes in libepb200.so (csrc/); importing fails loudly if the
 library has not been built.
 """
-from . import _lib  # noqa: F401  (loads libepb200.so or raises)
+import os as _os
+
+# The CPU proxy issues copies on its own streams while kernels spin on their
+# completion; CUDA multiplexes streams onto CUDA_DEVICE_MAX_CONNECTIONS hardware
+# queues (default 8), and a copy sharing a queue with such a kernel would wait
+# behind it.  More queues make that sharing unlikely; this only takes effect
+# if the package is imported before the process creates its CUDA context.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+from . import _lib  # noqa: F401,E402  (loads libepb200.so or raises)
 from .buffer import Buffer, Config, EventOverlap, LocalGroup, nvl_bytes_hint
 from .errors import (ChannelShutdown, ConfigError, ConnectionError_, EpsimError, FaultError, InvariantViolation,
                      ProtocolViolation, RingDeadlock, UnsupportedOperation)

@@ -41,13 +41,14 @@ P32 = C.POINTER(C.c_int32)
 
 class Config(C.Structure):
     _fields_ = [("nvl_bytes", C.c_size_t), ("ll_bytes", C.c_size_t), ("num_recv_slots", C.c_int),
-                ("fifo_channels", C.c_int), ("fifo_capacity", C.c_int), ("proxy_threads", C.c_int)]
+                ("fifo_channels", C.c_int), ("fifo_capacity", C.c_int), ("proxy_threads", C.c_int),
+                ("ht_transport", C.c_int)]
 
 
 class RecvLayout(C.Structure):
     _fields_ = [("cap_rows", i64), ("slot_bytes", i64), ("off_x", i64), ("off_scales", i64),
                 ("off_topk_idx", i64), ("off_topk_w", i64), ("off_src_idx", i64), ("comb_off", i64 * 2),
-                ("comb_w_off", i64), ("slot0_off", i64)]
+                ("comb_w_off", i64), ("slot0_off", i64), ("send_off", i64)]
 
 
 class DispatchArgs(C.Structure):

@@ -104,13 +104,16 @@ class Config:
         return nvl_bytes_hint(num_tokens, hidden_bytes // 2, num_ranks, num_topk, num_slots)
 
 
-def nvl_bytes_hint(num_tokens: int, hidden: int, num_ranks: int, num_topk: int = 8, num_slots: int = 3) -> int:
+def nvl_bytes_hint(num_tokens: int, hidden: int, num_ranks: int, num_topk: int = 8, num_slots: int = 3,
+                   ht_proxy: bool = False) -> int:
     """Arena bytes so that the worst case (every token to every rank) fits:
-    ``num_slots`` receive slots + 2 combine staging buffers of R*T rows."""
+    ``num_slots`` receive slots + 2 combine staging buffers of R*T rows (+ the
+    send-staging slot of the proxy transport)."""
     rows = num_ranks * num_tokens
     per_row = 2 * hidden + 4 * (hidden // 128) + 12 * num_topk + 4
     comb_row = 2 * hidden + 4 * num_topk
-    return rows * (num_slots * per_row + 2 * comb_row) + 256 * (6 * num_slots + 6) + (1 << 20)
+    slots = num_slots + (1 if ht_proxy else 0)
+    return rows * (slots * per_row + 2 * comb_row) + 256 * (6 * slots + 6) + (1 << 20)
 
 
 class _SlotMemory:
@@ -126,10 +129,11 @@ class _Rank:
     object (receive-slot pool, cached arena geometry)."""
 
     def __init__(self, rank: int, world: int, nvl_bytes: int, ll_bytes: int, num_recv_slots: int,
-                 fifo_channels: int, fifo_capacity: int, proxy_threads: int):
+                 fifo_channels: int, fifo_capacity: int, proxy_threads: int, ht_proxy: bool = False):
         self.rank, self.world = rank, world
         self.device = torch.device("cuda", torch.cuda.current_device())
-        cfg = L.Config(nvl_bytes, ll_bytes, num_recv_slots, fifo_channels, fifo_capacity, proxy_threads)
+        cfg = L.Config(nvl_bytes, ll_bytes, num_recv_slots, fifo_channels, fifo_capacity, proxy_threads,
+                       1 if ht_proxy else 0)
         ctx = C.c_void_p()
         check(lib.epb_create(C.byref(ctx), rank, world, C.byref(cfg)))
         self.ctx = ctx
@@ -245,21 +249,24 @@ class Buffer:
                  num_qps_per_rank: int = 24, allow_nvlink_for_low_latency_mode: bool = True,
                  allow_mnnvl: bool = False, explicitly_destroy: bool = False, *, num_recv_slots: int = 3,
                  fifo_channels: int = 8, fifo_capacity: int = 1024, proxy_threads: int = 4,
-                 ll_transport: str = "nvlink"):
+                 ll_transport: str = "nvlink", ht_transport: str = "nvlink"):
         import torch.distributed as dist
         if group is not None and dist.is_available() and dist.is_initialized():
             rank, world = dist.get_rank(group), dist.get_world_size(group)
         else:
             rank, world = 0, 1
-        if ll_transport not in ("nvlink", "proxy"):
-            raise ConfigError("ll_transport must be 'nvlink' or 'proxy'")
+        if ll_transport not in ("nvlink", "proxy") or ht_transport not in ("nvlink", "proxy"):
+            raise ConfigError("ll_transport / ht_transport must be 'nvlink' or 'proxy'")
+        if ht_transport == "proxy" and fifo_channels <= 0:
+            raise ConfigError("ht_transport='proxy' needs fifo_channels > 0")
+        self.ht_transport = ht_transport
         self.rank, self.group_size, self.group = rank, world, group
         self.low_latency_mode = low_latency_mode
         self.ll_transport = ll_transport
         self.num_nvl_bytes, self.num_rdma_bytes = int(num_nvl_bytes), int(num_rdma_bytes)
         ll_bytes = self.num_rdma_bytes if low_latency_mode else 0
         self._rank = _Rank(rank, world, max(self.num_nvl_bytes, 1 << 20), ll_bytes, num_recv_slots,
-                           fifo_channels, fifo_capacity, proxy_threads)
+                           fifo_channels, fifo_capacity, proxy_threads, ht_proxy=ht_transport == "proxy")
         if world > 1:
             h = (C.c_char * L.IPC_HANDLE_BYTES)()
             check(lib.epb_ipc_handle(self._rank.ctx, h))
@@ -269,7 +276,7 @@ class Buffer:
             dist.barrier(group=group)
         else:
             check(lib.epb_link_local(_ctx_array([self._rank]), 1))
-        if ll_transport == "proxy":
+        if ll_transport == "proxy" or ht_transport == "proxy":
             self.start_proxy()
         self._g = _Group([self._rank])
         self._native = self._rank.native
@@ -438,14 +445,17 @@ class LocalGroup:
 
     def __init__(self, world: int, num_nvl_bytes: int, num_rdma_bytes: int = 0, *, num_recv_slots: int = 3,
                  fifo_channels: int = 0, fifo_capacity: int = 1024, proxy_threads: int = 1,
-                 ll_transport: str = "nvlink"):
+                 ll_transport: str = "nvlink", ht_transport: str = "nvlink"):
         if world < 1 or world > L.MAX_LOCAL:
             raise ConfigError("LocalGroup world must be in [1, 8]")
+        if ht_transport == "proxy" and fifo_channels <= 0:
+            raise ConfigError("ht_transport='proxy' needs fifo_channels > 0")
         self.ranks = [_Rank(r, world, num_nvl_bytes, num_rdma_bytes, num_recv_slots, fifo_channels, fifo_capacity,
-                            proxy_threads) for r in range(world)]
+                            proxy_threads, ht_proxy=ht_transport == "proxy") for r in range(world)]
         check(lib.epb_link_local(_ctx_array(self.ranks), world))
         self.ll_transport = ll_transport
-        if ll_transport == "proxy":
+        self.ht_transport = ht_transport
+        if ll_transport == "proxy" or ht_transport == "proxy":
             for rk in self.ranks:
                 check(lib.epb_proxy_start(rk.ctx))
                 rk.proxy_running = True

@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "ctx.h"
+#include "ll_common.cuh"
 
 namespace epb {
 
@@ -27,6 +28,10 @@ constexpr int kCopyUnroll = 7;
 // ---------------------------------------------------------------------------
 struct CombineParams {
   int n_local;
+  int proxy;                     // ht_transport = CPU proxy: rows go back through the FIFO
+  int phase;                     // proxy: 1 = stage + hand rows to the proxy, 2 = reduce
+  int fifo_channels;
+  uint64_t ht_calls[kMaxLocal];  // proxy transport: expected ht_sig[1][src]
   uint32_t epoch[kMaxLocal];
   uint32_t expected[kMaxLocal];
   RankView rv[kMaxLocal];
@@ -116,6 +121,177 @@ __device__ __forceinline__ void zero_row(int4* out, int n16, int lane) {
   for (int i = lane; i < n16; i += 32) st_na_v4(out + i, make_int4(0, 0, 0, 0));
 }
 
+// Phase B: reduce my tokens.  pull: partial d is read in place from d's input
+// (over NVLink); else from my staging, where the sources pushed their rows.
+__device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bool pull, const int64_t* s_xoff,
+                                              const int64_t* s_woff, const int32_t* s_excl, const int32_t* s_mypre) {
+  const RankView& rv = P.rv[lr];
+  const epb_combine_args_t& a = P.a[lr];
+  const int R = rv.world, me = rv.rank, nb = gridDim.x, b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const int par = P.epoch[lr] & 1;
+  const int k = a.num_topk;
+  const size_t row_bytes = (size_t)a.hidden * 2;
+  const int n16 = (int)(row_bytes >> 4);
+  const char* my_stage = rv.base + P.lay.comb_off[par];
+  const int T = a.num_tokens;
+  const int Tb = (T + nb - 1) / nb;
+  const int tb0 = b * Tb, tb1 = min(T, tb0 + Tb);
+  __shared__ RowSrc rs;
+  if (tid == 0) rs.row_bytes = row_bytes;
+  if (tid < kMaxRanks) {
+    const int d = tid;
+    if (d == me) {
+      rs.base[d] = static_cast<const char*>(a.x);
+      rs.wbase[d] = reinterpret_cast<const char*>(a.topk_weights);
+      rs.row0[d] = s_excl[me];
+    } else if (pull) {
+      rs.base[d] = d < R ? rv.peer[d] + s_xoff[d] : nullptr;
+      rs.wbase[d] = (d < R && s_woff[d] >= 0) ? rv.peer[d] + s_woff[d] : nullptr;
+      rs.row0[d] = (d < R && me > 0) ? a.rank_prefix_matrix[(me - 1) * R + d] : 0;  // my first row at d
+    } else {
+      rs.base[d] = my_stage;
+      rs.wbase[d] = my_stage + P.lay.comb_w_off;
+      rs.row0[d] = s_mypre[d];
+    }
+  }
+  __syncthreads();
+  for (int t = tb0 + warp; t < tb1; t += nwarps) {
+    const int32_t* sh = a.send_head + (size_t)t * R;
+    // contributing ranks as a bitmask; rows are taken in ascending rank order
+    // (the canonical sum order) via __fns inside reduce_rows
+    uint32_t mask = 0;
+    if (lane < R && sh[lane] >= 0) mask = 1u << lane;
+    mask = __reduce_or_sync(0xffffffffu, mask);
+    int4* out = reinterpret_cast<int4*>(static_cast<char*>(a.combined_x) + (size_t)t * row_bytes);
+    switch (__popc(mask)) {
+      case 1: reduce_rows<1>(rs, mask, sh, out, n16, lane); break;
+      case 2: reduce_rows<2>(rs, mask, sh, out, n16, lane); break;
+      case 3: reduce_rows<3>(rs, mask, sh, out, n16, lane); break;
+      case 4: reduce_rows<4>(rs, mask, sh, out, n16, lane); break;
+      case 5: reduce_rows<5>(rs, mask, sh, out, n16, lane); break;
+      case 6: reduce_rows<6>(rs, mask, sh, out, n16, lane); break;
+      case 7: reduce_rows<7>(rs, mask, sh, out, n16, lane); break;
+      case 8: reduce_rows<8>(rs, mask, sh, out, n16, lane); break;
+      default: zero_row(out, n16, lane); break;
+    }
+    if (a.combined_topk_weights != nullptr && lane < k) {
+      float w = 0.0f;
+      for (uint32_t m = mask; m != 0; m &= m - 1) {
+        const int d = __ffs(m) - 1;
+        const float* wsrc = reinterpret_cast<const float*>(rs.wbase[d]);
+        if (wsrc != nullptr) w = __fadd_rn(w, wsrc[(size_t)(rs.row0[d] + sh[d]) * k + lane]);
+      }
+      a.combined_topk_weights[(size_t)t * k + lane] = w;
+    }
+  }
+}
+
+// Proxy transport (PAPER.md:142 hierarchical reduce, data moved by the CPU
+// proxy): each source's rows are contiguous in my receive order, so one WRITE
+// per source (rows, then weights) lands them at the mirror position in the
+// source's staging, followed by an ATOMIC on its ht_sig[1][me].  Inputs inside
+// my region are sent in place; others are first copied to my send staging.
+__device__ __noinline__ void push_combine_cmds(const CombineParams& P, int lr, const int32_t (*s_cnt)[kMaxRanks],
+                                               const int32_t* s_excl, const int32_t* s_sendpre, int64_t x_src,
+                                               int64_t w_src, bool aborted) {
+  const RankView& rv = P.rv[lr];
+  const epb_combine_args_t& a = P.a[lr];
+  const int R = rv.world, me = rv.rank, par = P.epoch[lr] & 1, k = a.num_topk;
+  const int64_t arena = (int64_t)kRegionHeader, row_bytes = (int64_t)a.hidden * 2;
+  for (int s = 0; s < R; ++s) {
+    if (s == me) continue;
+    const int ch = s % P.fifo_channels;
+    const int64_t cnt = s_cnt[s][me];
+    uint64_t lo, hi;
+    if (!aborted && cnt > 0) {
+      const int64_t dst = P.lay.comb_off[par] - arena;
+      cmd_pack_dev(EPB_CMD_WRITE, s, ch, x_src + s_excl[s] * row_bytes, dst + s_sendpre[s] * row_bytes,
+                   cnt * row_bytes, 0, lo, hi);
+      if (fifo_push(rv, ch, lo, hi) < 0) return;
+      if (w_src >= 0 && k > 0) {
+        cmd_pack_dev(EPB_CMD_WRITE, s, ch, w_src + (int64_t)s_excl[s] * k * 4,
+                     dst + P.lay.comb_w_off + (int64_t)s_sendpre[s] * k * 4, cnt * k * 4, 0, lo, hi);
+        if (fifo_push(rv, ch, lo, hi) < 0) return;
+      }
+    }
+    cmd_pack_dev(EPB_CMD_ATOMIC, s, ch, 0, offsetof(Meta, ht_sig) + sizeof(uint64_t) * (kMaxRanks + me), 1, 0, lo,
+                 hi);
+    if (fifo_push(rv, ch, lo, hi) < 0) return;
+  }
+}
+
+__device__ __forceinline__ void combine_via_proxy(const CombineParams& P, int lr, const int32_t (*s_cnt)[kMaxRanks],
+                                                  const int32_t* s_excl, const int32_t* s_sendpre, bool abort) {
+  const RankView& rv = P.rv[lr];
+  const epb_combine_args_t& a = P.a[lr];
+  const int R = rv.world, me = rv.rank, nb = gridDim.x, b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const int N = a.num_recv, k = a.num_topk;
+  const size_t row_bytes = (size_t)a.hidden * 2;
+  const int n16 = (int)(row_bytes >> 4);
+  Scratch* sc = scratch_of(rv.base);
+  const char* xp = static_cast<const char*>(a.x);
+  const char* wp = reinterpret_cast<const char*>(a.topk_weights);
+  const char* lo = rv.base + kRegionHeader;
+  const char* hi = rv.base + rv.region_bytes;
+  const bool in_place = xp >= lo && xp + (size_t)N * row_bytes <= hi &&
+                        (wp == nullptr || (wp >= lo && wp + (size_t)N * k * 4 <= hi));
+  char* stage = rv.base + P.lay.send_off;
+  if (!abort && !in_place) {
+    // the previous dispatch's WRITEs read this staging: wait until the proxy
+    // has completed every command pushed so far
+    if (tid < P.fifo_channels) {
+      const int64_t* ctl = reinterpret_cast<const int64_t*>(sc->fifo_ctl[tid]);
+      const int64_t want = sc->fifo_tail[tid];
+      uint64_t t0 = 0;
+      while (ld_acquire_sys(ctl + EPB_CTL_COMPLETED) < want) {
+        const uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > rv.timeout_ns) {
+          report_error(rv, EPB_ERR_DEADLOCK, 0x340 + tid);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    const int Jb = (N + nb - 1) / nb;
+    const int j0 = b * Jb, j1 = min(N, j0 + Jb);
+    for (int j = j0 + warp; j < j1; j += nwarps) {
+      int s = 0;
+      while (s < R - 1 && j >= s_excl[s] + s_cnt[s][me]) ++s;
+      if (s == me) continue;  // my own partials are reduced in place
+      const int4* src = reinterpret_cast<const int4*>(xp + (size_t)j * row_bytes);
+      int4* dst = reinterpret_cast<int4*>(stage + P.lay.off_x + (size_t)j * row_bytes);
+      for (int i = lane; i < n16; i += 32) st_v4(dst + i, ld_nc_v4(src + i));
+      if (wp != nullptr && lane < k)
+        reinterpret_cast<float*>(stage + P.lay.off_topk_w)[(size_t)j * k + lane] = a.topk_weights[(size_t)j * k + lane];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t old = atom_add_acq_rel_gpu(&meta_of(rv.base)->comb_done[me], 1u);
+    if (old + 1 == P.expected[lr]) {  // the last of my blocks hands the rows to the proxy
+      const int64_t arena = (int64_t)kRegionHeader;
+      const int64_t x_src = in_place ? (int64_t)(xp - rv.base) - arena : P.lay.send_off + P.lay.off_x - arena;
+      const int64_t w_src = wp == nullptr ? -1
+                            : in_place ? (int64_t)(wp - rv.base) - arena
+                                       : P.lay.send_off + P.lay.off_topk_w - arena;
+      push_combine_cmds(P, lr, s_cnt, s_excl, s_sendpre, x_src, w_src, abort);
+    }
+  }
+}
+
+// Proxy transport, between the two combine launches: one block per local rank
+// waits until every source's rows (and its ATOMIC) have landed.  The copies
+// run on the proxy's streams while only these blocks are resident.
+__global__ void combine_proxy_wait_kernel(const __grid_constant__ CombineParams P) {
+  const RankView& rv = P.rv[blockIdx.x];
+  const int tid = threadIdx.x;
+  if (tid < rv.world && tid != rv.rank)
+    wait_geq64(rv, &meta_of(rv.base)->ht_sig[1][tid], P.ht_calls[blockIdx.x], 0x320 + tid, 500);
+}
+
 __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __grid_constant__ CombineParams P) {
   const int lr = blockIdx.y;
   const RankView& rv = P.rv[lr];
@@ -159,6 +335,18 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   // and no staging pass; otherwise rows are pushed back into staging first.
   const int N = a.num_recv;
   __shared__ int64_t s_xoff[kMaxRanks], s_woff[kMaxRanks];
+  if (P.proxy) {  // proxy transport: no SM access to peers' memory at all
+    if (P.phase == 1) {
+      combine_via_proxy(P, lr, s_cnt, s_excl, s_sendpre, abort);
+      trace_mark(rv, 17);
+    } else if (!abort) {
+      trace_mark_max(rv, 21);
+      reduce_tokens(P, lr, false, s_xoff, s_woff, s_excl, s_mypre);
+      trace_mark(rv, 19);
+      trace_mark_max(rv, 20);
+    }
+    return;
+  }
   if (b == 0 && tid < R) {  // my offsets to every peer: tagged words (16-byte / 4-byte units)
     const char* xp = static_cast<const char*>(a.x);
     const char* wp = reinterpret_cast<const char*>(a.topk_weights);
@@ -228,59 +416,7 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   trace_mark_max(rv, 21);
   if (abort) return;
 
-  // phase B: reduce my tokens
-  const char* my_stage = rv.base + P.lay.comb_off[par];
-  const int T = a.num_tokens;
-  const int Tb = (T + nb - 1) / nb;
-  const int tb0 = b * Tb, tb1 = min(T, tb0 + Tb);
-  __shared__ RowSrc rs;
-  if (tid == 0) rs.row_bytes = row_bytes;
-  if (tid < kMaxRanks) {
-    const int d = tid;
-    if (d == me) {
-      rs.base[d] = static_cast<const char*>(a.x);
-      rs.wbase[d] = reinterpret_cast<const char*>(a.topk_weights);
-      rs.row0[d] = s_excl[me];
-    } else if (pull) {
-      rs.base[d] = d < R ? rv.peer[d] + s_xoff[d] : nullptr;
-      rs.wbase[d] = (d < R && s_woff[d] >= 0) ? rv.peer[d] + s_woff[d] : nullptr;
-      rs.row0[d] = (d < R && me > 0) ? a.rank_prefix_matrix[(me - 1) * R + d] : 0;  // my first row at d
-    } else {
-      rs.base[d] = my_stage;
-      rs.wbase[d] = my_stage + P.lay.comb_w_off;
-      rs.row0[d] = s_mypre[d];
-    }
-  }
-  __syncthreads();
-  for (int t = tb0 + warp; t < tb1; t += nwarps) {
-    const int32_t* sh = a.send_head + (size_t)t * R;
-    // contributing ranks as a bitmask; rows are taken in ascending rank order
-    // (the canonical sum order) via __fns inside reduce_rows
-    uint32_t mask = 0;
-    if (lane < R && sh[lane] >= 0) mask = 1u << lane;
-    mask = __reduce_or_sync(0xffffffffu, mask);
-    int4* out = reinterpret_cast<int4*>(static_cast<char*>(a.combined_x) + (size_t)t * row_bytes);
-    switch (__popc(mask)) {
-      case 1: reduce_rows<1>(rs, mask, sh, out, n16, lane); break;
-      case 2: reduce_rows<2>(rs, mask, sh, out, n16, lane); break;
-      case 3: reduce_rows<3>(rs, mask, sh, out, n16, lane); break;
-      case 4: reduce_rows<4>(rs, mask, sh, out, n16, lane); break;
-      case 5: reduce_rows<5>(rs, mask, sh, out, n16, lane); break;
-      case 6: reduce_rows<6>(rs, mask, sh, out, n16, lane); break;
-      case 7: reduce_rows<7>(rs, mask, sh, out, n16, lane); break;
-      case 8: reduce_rows<8>(rs, mask, sh, out, n16, lane); break;
-      default: zero_row(out, n16, lane); break;
-    }
-    if (a.combined_topk_weights != nullptr && lane < k) {
-      float w = 0.0f;
-      for (uint32_t m = mask; m != 0; m &= m - 1) {
-        const int d = __ffs(m) - 1;
-        const float* wsrc = reinterpret_cast<const float*>(rs.wbase[d]);
-        if (wsrc != nullptr) w = __fadd_rn(w, wsrc[(size_t)(rs.row0[d] + sh[d]) * k + lane]);
-      }
-      a.combined_topk_weights[(size_t)t * k + lane] = w;
-    }
-  }
+  reduce_tokens(P, lr, pull, s_xoff, s_woff, s_excl, s_mypre);
   trace_mark(rv, 19);
   trace_mark_max(rv, 20);
   if (pull) {
@@ -300,6 +436,11 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
   CombineParams P;
   std::memset(&P, 0, sizeof(P));
   P.n_local = n_local;
+  P.proxy = ctxs[0]->cfg.ht_transport ? 1 : 0;
+  P.fifo_channels = ctxs[0]->cfg.fifo_channels;
+  for (int i = 0; i < n_local; ++i)
+    if (P.proxy && (ctxs[i]->cfg.fifo_channels <= 0 || !ctxs[i]->proxy || !ctxs[i]->cfg.ht_transport))
+      return epb_set_error(EPB_ERR_CONFIG, "ht_transport=proxy needs FIFO channels and a running proxy on every rank");
   int nb = std::max(1, num_sms / n_local);
   const int max_active = epb_max_active_blocks((const void*)combine_kernel, kCombineThreads, 0);
   nb = std::min(nb, std::max(1, max_active * ctxs[0]->num_sms / n_local));
@@ -310,11 +451,21 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     P.epoch[i] = ++c->comb_epoch;
     c->comb_cum += (uint32_t)nb;
     P.expected[i] = c->comb_cum;
+    if (P.proxy) P.ht_calls[i] = ++c->ht_comb_calls;
     P.rv[i] = c->view();
     P.a[i] = a;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* kargs[] = {&P};
+  if (P.proxy) {  // stage + push | wait for the peers' rows | reduce
+    P.phase = 1;
+    EPB_CUDA(cudaLaunchKernel((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
+    combine_proxy_wait_kernel<<<n_local, 32, 0, st>>>(P);
+    EPB_CUDA(cudaGetLastError());
+    P.phase = 2;
+    EPB_CUDA(cudaLaunchKernel((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
+    return EPB_OK;
+  }
   EPB_CUDA(epb_launch_grid_sync((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
   return EPB_OK;
 }

@@ -56,6 +56,7 @@ struct Meta {
   uint64_t ll_disp_flag[2][kMaxRanks];   // LL dispatch: epoch stamp per src
   uint64_t ll_comb_flag[2][kMaxRanks];   // LL combine: epoch stamp per src
   uint64_t proxy_sig[kMaxFifo][kMaxRanks];  // CPU-proxy signals: += 1 per piggybacked WRITE from src on channel
+  uint64_t ht_sig[2][kMaxRanks];         // proxy HT transport: src's ATOMIC += 1 per [dispatch|combine] call
   // combine mode message (tagged words): where src's input rows / weights live
   // inside src's region, in 16-byte / 4-byte units (kNotifyAbort: not there)
   uint64_t comb_msg[2][kMaxRanks][2];
@@ -68,7 +69,10 @@ struct Scratch {                         // private to the owning rank
   // dispatch, between the blocks of one rank (tagged words, this call's epoch):
   uint64_t ch_cnt[kMaxRanks][kMaxChannels];   // my tokens per (destination, channel)
   uint64_t ch_excl[kMaxRanks][kMaxChannels];  // exclusive prefix over channels of ch_cnt
-  uint64_t plan[2][kMaxRanks];                // [0][d]: d's receive slot (kNotifyAbort: aborted), [1][d]: my first row at d
+  // plan[0][d]: d's receive slot (kNotifyAbort: aborted), [1][d]: my first row
+  // at d, [2][d]: rows I send to d, [3][d]: where they start in my send
+  // staging (proxy transport)
+  uint64_t plan[4][kMaxRanks];
   uint32_t ll_ticket[4];                 // LL last-warp tickets: [dispatch|combine][parity]
   // LL epochs live on the device (bumped by each call's last warp) so LL calls
   // can be captured in CUDA graphs and replayed: [dispatch|combine]
@@ -332,10 +336,14 @@ __device__ __forceinline__ bool wait_geq_gpu(const RankView& rv, const uint32_t*
   }
   return true;
 }
-__device__ __forceinline__ bool wait_geq64(const RankView& rv, const uint64_t* p, uint64_t target, int64_t tag) {
+// sleep_ns > 0: __nanosleep between polls (counters written by a copy engine
+// on the proxy's behalf: a tight acquire loop on the line it writes slows it).
+__device__ __forceinline__ bool wait_geq64(const RankView& rv, const uint64_t* p, uint64_t target, int64_t tag,
+                                           unsigned sleep_ns = 0) {
   uint64_t t0 = 0;
   int iter = 0;
   while (static_cast<int64_t>(ld_acquire_sys(p) - target) < 0) {
+    if (sleep_ns) __nanosleep(sleep_ns);
     if ((++iter & 1023) == 0) {
       uint64_t now = globaltimer();
       if (t0 == 0) t0 = now;

@@ -22,6 +22,7 @@ struct epb_ctx {
   epb::HostInfo* host_dev = nullptr;    // device alias
   uint32_t disp_epoch = 0, comb_epoch = 0, ll_disp_epoch = 0, ll_comb_epoch = 0;
   uint32_t disp_cum = 0, comb_cum = 0;  // cumulative expected block signals per source
+  uint64_t ht_disp_calls = 0, ht_comb_calls = 0;  // proxy transport calls so far (ht_sig targets)
   uint64_t ll_proxy_disp = 0, ll_proxy_comb = 0;  // proxy-transport LL calls so far (signal targets)
   int num_sms = 148;
   uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;

@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "ctx.h"
+#include "ll_common.cuh"
 
 namespace epb {
 
@@ -65,6 +66,9 @@ __device__ __forceinline__ int warp_scan_row(const int32_t* in, int32_t* incl_ou
 
 struct DispatchParams {
   int n_local, num_slots;
+  int proxy;                    // ht_transport = CPU proxy (rows to peers go through the FIFO)
+  int fifo_channels;
+  uint64_t ht_calls[kMaxLocal];  // proxy transport: expected ht_sig[0][src] (calls so far)
   uint32_t epoch[kMaxLocal];   // per-call epoch: the tag of this call's mailbox / host words
   uint32_t target[kMaxLocal];  // cumulative done target (sum of grid widths so far)
   RankView rv[kMaxLocal];
@@ -300,8 +304,15 @@ __device__ __forceinline__ void exchange_counts(const DispatchParams& P, int lr,
   __syncwarp();
   const int ab = *s_abort;
   if (lane < R) {
-    st_relaxed_sys(&sc->plan[0][lane], tagged(ab ? kNotifyAbort : (uint32_t)s_slot[lane], epoch));
-    st_relaxed_sys(&sc->plan[1][lane], tagged((uint32_t)(me > 0 ? s_rpm[me - 1][lane] : 0), epoch));
+    const int d = lane;
+    const int mine = s_rpm[me][d] - (me > 0 ? s_rpm[me - 1][d] : 0);
+    int pre = 0;  // send-staging start: my rows to lower peers (the local destination is written in place)
+    for (int q = 0; q < d; ++q)
+      if (q != me) pre += s_rpm[me][q] - (me > 0 ? s_rpm[me - 1][q] : 0);
+    st_relaxed_sys(&sc->plan[0][d], tagged(ab ? kNotifyAbort : (uint32_t)s_slot[d], epoch));
+    st_relaxed_sys(&sc->plan[1][d], tagged((uint32_t)(me > 0 ? s_rpm[me - 1][d] : 0), epoch));
+    st_relaxed_sys(&sc->plan[2][d], tagged((uint32_t)mine, epoch));
+    st_relaxed_sys(&sc->plan[3][d], tagged((uint32_t)pre, epoch));
   }
   if (lane == 0) {
     sc->abort = ab;
@@ -310,6 +321,42 @@ __device__ __forceinline__ void exchange_counts(const DispatchParams& P, int lr,
   }
   trace_mark(rv, 5);
   for (int i = lane; i < R * R; i += 32) a.rank_prefix_matrix[i] = s_rpm[i / R][i % R];
+}
+
+// Proxy transport: WRITE TransferCmds (command.py layout, offsets relative to
+// the arena start) for every array of the rows I send to each peer, then one
+// ATOMIC (+1 on the peer's ht_sig[0][me]) — sent even for zero rows or an
+// aborted call, so the per-source counters stay in step with the calls.
+__device__ __noinline__ void push_dispatch_cmds(const DispatchParams& P, int lr, const int32_t* slot,
+                                                const int32_t* base, const int32_t* mine, const int32_t* pre,
+                                                bool aborted) {
+  const RankView& rv = P.rv[lr];
+  const epb_dispatch_args_t& a = P.a[lr];
+  const int R = rv.world, me = rv.rank;
+  const epb_recv_layout_t& Lo = P.lay;
+  const int64_t arena = (int64_t)kRegionHeader;
+  const int64_t row_bytes = (int64_t)a.hidden * a.elem_bytes;
+  const int64_t sizes[5] = {row_bytes, (int64_t)a.num_scales * 4, (a.topk_idx ? (int64_t)a.num_topk * 8 : 0),
+                            (a.topk_idx && a.topk_weights ? (int64_t)a.num_topk * 4 : 0), 4};
+  const int64_t offs[5] = {Lo.off_x, Lo.off_scales, Lo.off_topk_idx, Lo.off_topk_w, Lo.off_src_idx};
+  for (int d = 0; d < R; ++d) {
+    if (d == me) continue;
+    const int ch = d % P.fifo_channels;
+    uint64_t lo, hi;
+    if (!aborted && mine[d] > 0) {
+      const int64_t src_slot = Lo.send_off - arena;
+      const int64_t dst_slot = Lo.slot0_off + (int64_t)slot[d] * Lo.slot_bytes - arena;
+      for (int f = 0; f < 5; ++f) {
+        if (sizes[f] == 0) continue;
+        const int64_t so = src_slot + offs[f] + (int64_t)pre[d] * sizes[f];
+        const int64_t dof = dst_slot + offs[f] + (int64_t)base[d] * sizes[f];
+        cmd_pack_dev(EPB_CMD_WRITE, d, ch, so, dof, (int64_t)mine[d] * sizes[f], 0, lo, hi);
+        if (fifo_push(rv, ch, lo, hi) < 0) return;
+      }
+    }
+    cmd_pack_dev(EPB_CMD_ATOMIC, d, ch, 0, offsetof(Meta, ht_sig) + sizeof(uint64_t) * me, 1, 0, lo, hi);
+    if (fifo_push(rv, ch, lo, hi) < 0) return;
+  }
 }
 
 __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __grid_constant__ DispatchParams P) {
@@ -327,6 +374,7 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   __shared__ char* s_dst[kMaxRanks];
   __shared__ int32_t s_rb[kMaxRanks];
   __shared__ int32_t s_chx[kMaxRanks];
+  __shared__ int32_t s_slotv[kMaxRanks], s_base[kMaxRanks], s_mine[kMaxRanks], s_pre[kMaxRanks];
   __shared__ int s_abort;
   trace_mark(rv, 0);
   if (tid == 0) s_abort = 0;
@@ -356,22 +404,36 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     __syncthreads();
   }
   if (warp == 0) {
-    for (int i = lane; i < 3 * R; i += 32) {
+    const int nf = P.proxy ? 5 : 3;  // slot, row base, channel offset (+ my count, staging start)
+    for (int i = lane; i < nf * R; i += 32) {
       const int d = i % R, f = i / R;
-      const uint64_t* w = f == 0 ? &sc->plan[0][d] : f == 1 ? &sc->plan[1][d] : &sc->ch_excl[d][c];
+      const uint64_t* w = f == 2 ? &sc->ch_excl[d][c] : &sc->plan[f < 2 ? f : f - 1][d];
       const uint32_t v = wait_tagged(rv, w, epoch, 0x190, c == 0 ? 0 : 64);
       if (f == 0) {
         if (v == kNotifyAbort) s_abort = EPB_ERR_CONFIG;
-        else s_dst[d] = rv.peer[d] + P.lay.slot0_off + (int64_t)v * P.lay.slot_bytes;
+        s_slotv[d] = (int)v;
       } else if (f == 1) {
-        s_rb[d] = (int)v;
-      } else {
+        s_base[d] = (int)v;
+      } else if (f == 2) {
         s_chx[d] = (int)v;
+      } else if (f == 3) {
+        s_mine[d] = (int)v;
+      } else {
+        s_pre[d] = (int)v;
       }
     }
   }
   __syncthreads();
-  if (tid < R) s_rb[tid] += s_chx[tid];  // first row of this channel's run at tid
+  if (tid < R && !s_abort) {
+    const int d = tid;
+    if (P.proxy && d != me) {  // rows for a peer go to my send staging, in the peer's order
+      s_dst[d] = rv.base + P.lay.send_off;
+      s_rb[d] = s_pre[d] + s_chx[d];
+    } else {
+      s_dst[d] = rv.peer[d] + P.lay.slot0_off + (int64_t)s_slotv[d] * P.lay.slot_bytes;
+      s_rb[d] = s_base[d] + s_chx[d];  // first row of this channel's run at d
+    }
+  }
   __syncthreads();
   trace_mark(rv, 7);
   trace_mark_max(rv, 11);
@@ -438,11 +500,26 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   __syncthreads();
   trace_mark(rv, 9);
   trace_mark_max(rv, 12);
-  if (tid < R) {  // the local destination only needs gpu scope
-    if (tid == me) red_release_gpu_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
-    else red_release_sys_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
+  if (!P.proxy) {
+    if (tid < R) {  // the local destination only needs gpu scope
+      if (tid == me) red_release_gpu_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
+      else red_release_sys_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
+    }
+    if (c == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->disp_done[tid], P.target[lr], 0x200 + tid);
+  } else {
+    // proxy transport: the last of my blocks to finish hands the peers' rows
+    // to the CPU proxy — one WRITE per array and destination (contiguous in
+    // my staging and in the peer's slot), then an ATOMIC on the peer's
+    // ht_sig[0][me]; FIFO order on the channel puts the data first
+    if (tid == 0) {
+      const uint32_t old = atom_add_acq_rel_gpu(&meta_of(rv.base)->disp_done[me], 1u);
+      if (old + 1 == P.target[lr]) push_dispatch_cmds(P, lr, s_slotv, s_base, s_mine, s_pre, s_abort != 0);
+    }
+    if (c == 0 && tid < R) {
+      if (tid == me) wait_geq(rv, &meta_of(rv.base)->disp_done[me], P.target[lr], 0x200 + tid);
+      else wait_geq64(rv, &meta_of(rv.base)->ht_sig[0][tid], P.ht_calls[lr], 0x220 + tid, 500);
+    }
   }
-  if (c == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->disp_done[tid], P.target[lr], 0x200 + tid);
   trace_mark(rv, 10);
 }
 
@@ -459,6 +536,14 @@ extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_
   std::memset(&P, 0, sizeof(P));
   P.n_local = n_local;
   P.num_slots = std::max(1, ctxs[0]->cfg.num_recv_slots);
+  P.proxy = ctxs[0]->cfg.ht_transport ? 1 : 0;
+  P.fifo_channels = ctxs[0]->cfg.fifo_channels;
+  for (int i = 0; i < n_local; ++i) {
+    if ((ctxs[i]->cfg.ht_transport != 0) != (P.proxy != 0))
+      return epb_set_error(EPB_ERR_CONFIG, "all ranks of a group must use the same ht_transport");
+    if (P.proxy && (ctxs[i]->cfg.fifo_channels <= 0 || !ctxs[i]->proxy))
+      return epb_set_error(EPB_ERR_CONFIG, "ht_transport=proxy needs FIFO channels and a running proxy");
+  }
   int max_tc = 1;
   for (int i = 0; i < n_local; ++i) {
     const epb_dispatch_args_t& a = args[i];
@@ -481,6 +566,7 @@ extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_
     P.epoch[i] = ++c->disp_epoch;
     c->disp_cum += (uint32_t)num_channels;
     P.target[i] = c->disp_cum;
+    if (P.proxy) P.ht_calls[i] = ++c->ht_disp_calls;
     P.rv[i] = c->view();
     P.a[i] = args[i];
   }

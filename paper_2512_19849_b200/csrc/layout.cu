@@ -101,9 +101,10 @@ int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t
   const size_t per_row = x_row + S * 4 + (size_t)k * 12 + 4;
   const size_t comb_row = 2 * (size_t)hidden + (size_t)k * 4;
   const int ns = std::max(1, ctx->cfg.num_recv_slots);
-  const size_t overhead = A * (size_t)(6 * ns + 6);
+  const int nsend = ctx->cfg.ht_transport ? 1 : 0;  // proxy transport: one send-staging slot
+  const size_t overhead = A * (size_t)(6 * (ns + nsend) + 6);
   if (ctx->cfg.nvl_bytes <= overhead) return epb_set_error(EPB_ERR_CONFIG, "num_nvl_bytes too small");
-  int64_t cap = (int64_t)((ctx->cfg.nvl_bytes - overhead) / (ns * per_row + 2 * comb_row));
+  int64_t cap = (int64_t)((ctx->cfg.nvl_bytes - overhead) / ((ns + nsend) * per_row + 2 * comb_row));
   cap &= ~(int64_t)15;
   if (cap <= 0) return epb_set_error(EPB_ERR_CONFIG, "num_nvl_bytes too small for this hidden size");
   std::memset(L, 0, sizeof(*L));
@@ -119,8 +120,13 @@ int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t
   L->comb_w_off = align_up(cap * 2 * (size_t)hidden, A);
   L->comb_off[0] = L->slot0_off + ns * L->slot_bytes;
   L->comb_off[1] = L->comb_off[0] + comb_bytes;
-  if ((size_t)(L->comb_off[1] + comb_bytes - L->slot0_off) > ctx->cfg.nvl_bytes)
+  L->send_off = nsend ? L->comb_off[1] + comb_bytes : 0;
+  const int64_t end = nsend ? L->send_off + L->slot_bytes : L->comb_off[1] + comb_bytes;
+  if ((size_t)(end - L->slot0_off) > ctx->cfg.nvl_bytes)
     return epb_set_error(EPB_ERR_CONFIG, "internal: recv layout exceeds arena");
+  // proxy TransferCmd offsets are 32-bit, relative to the arena start (proxy.cpp)
+  if (nsend && (uint64_t)(ctx->ll_off() - epb::kRegionHeader + ctx->cfg.ll_bytes) > 0xFFFFFFFFull)
+    return epb_set_error(EPB_ERR_CONFIG, "proxy transport needs num_nvl_bytes + num_rdma_bytes < 4 GiB");
   return EPB_OK;
 }
 

@@ -218,8 +218,9 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
           int rows = 0;
           for (int le = 0; le < L; ++le) rows += cnt[d * L + le];
           const int ch = d % P.disp_channels;
-          const int64_t src_off = g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
-          const int64_t dst_off = g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
+          const int64_t rel = P.ll_off - (int64_t)kRegionHeader;  // commands address the arena start
+          const int64_t src_off = rel + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
+          const int64_t dst_off = rel + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
           const int64_t len = g.hdr_bytes + (int64_t)rows * rstride;
           uint64_t lo, hi;
           cmd_pack_dev(EPB_CMD_WRITE, d, ch, src_off, dst_off, len, EPB_FLAG_PIGGYBACK_ATOMIC, lo, hi);
@@ -369,8 +370,9 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
           int64_t rows = 0;
           for (int le = 0; le < L; ++le) rows += a.packed_recv_layout_range[le * R + s] & 0xffffffffll;
           const int ch = P.disp_channels + s % P.disp_channels;
-          const int64_t src_off = g.off_comb_send + (int64_t)(par * R + s) * g.comb_block;
-          const int64_t dst_off = g.off_comb_recv + (int64_t)(par * R + me) * g.comb_block;
+          const int64_t rel = P.ll_off - (int64_t)kRegionHeader;  // commands address the arena start
+          const int64_t src_off = rel + g.off_comb_send + (int64_t)(par * R + s) * g.comb_block;
+          const int64_t dst_off = rel + g.off_comb_recv + (int64_t)(par * R + me) * g.comb_block;
           uint64_t lo, hi;
           cmd_pack_dev(EPB_CMD_WRITE, s, ch, src_off, dst_off, rows * g.comb_row, EPB_FLAG_PIGGYBACK_ATOMIC, lo, hi);
           fifo_push(rv, ch, lo, hi);
@@ -489,6 +491,9 @@ static int ll_check(epb_ctx* c, const LLGeom& g) {
     return epb_set_error(EPB_ERR_CONFIG, "low-latency region too small: need " + std::to_string(g.bytes_needed) +
                                              " bytes, have " + std::to_string(c->cfg.ll_bytes));
   if (g.E / g.R > kMaxLocalExperts) return epb_set_error(EPB_ERR_CONFIG, "too many local experts");
+  if (c->cfg.fifo_channels > 0 && c->ll_off() - kRegionHeader + c->cfg.ll_bytes > 0xFFFFFFFFull)
+    return epb_set_error(EPB_ERR_CONFIG, "proxy transport: 32-bit TransferCmd offsets need "
+                                         "num_nvl_bytes + num_rdma_bytes < 4 GiB");
   return EPB_OK;
 }
 

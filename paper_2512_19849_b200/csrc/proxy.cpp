@@ -9,10 +9,13 @@
 //
 // Proxy: proxy_threads OS threads per
 // rank; thread i owns channels {c : c % threads == i} and never shares mutable
-// state with another thread.  Each owned channel has its own
-// CUDA stream, so commands of one channel take effect in FIFO order while
-// channels proceed independently ("cross-FIFO ordering is not guaranteed").
-//   WRITE   -> offset translation (symmetric LL region) and a
+// state with another thread.  Each thread issues on its own
+// CUDA stream, so commands of one channel take effect in FIFO order (channels
+// of one thread are additionally ordered among themselves, which "cross-FIFO
+// ordering is not guaranteed" permits).
+//   WRITE   -> offset translation (the symmetric data region — normal arena, then
+//              the LL region — starting after the Meta/Scratch header;
+//              SPEC.md:237-241) and a
 //              cudaMemcpyAsync; contiguous WRITEs to the same peer coalesce
 //              into one copy; FLAG_PIGGYBACK_ATOMIC then bumps the receiver's
 //              proxy_sig[channel][me] counter on the same stream (ordered after
@@ -115,13 +118,14 @@ void serve(epb_proxy* px, ChanState& cs, std::unordered_map<uint64_t, uint64_t>&
   }
   switch (kind) {
     case EPB_CMD_WRITE: {
-      const size_t ll = ctx->cfg.ll_bytes;
-      if (so + len > ll || dof + len > ll) {  // FaultError(rank, offset, length), errors.py:20-27
-        proxy_error(ctx, EPB_ERR_FAULT, (int64_t)((uint64_t)dst << 56 | (so + len > ll ? so : dof)));
+      // offsets are relative to the arena start (normal arena, then the LL region)
+      const size_t data = ctx->ll_off() - epb::kRegionHeader + ctx->cfg.ll_bytes;
+      if (so + len > data || dof + len > data) {  // FaultError(rank, offset, length), errors.py:20-27
+        proxy_error(ctx, EPB_ERR_FAULT, (int64_t)((uint64_t)dst << 56 | (so + len > data ? so : dof)));
         return;
       }
-      char* s = ctx->base + ctx->ll_off() + so;
-      char* d = ctx->peer[dst] + ctx->ll_off() + dof;
+      char* s = ctx->base + epb::kRegionHeader + so;
+      char* d = ctx->peer[dst] + epb::kRegionHeader + dof;
       PendingCopy& p = cs.pend;
       if (p.len > 0 && p.dst == dst && p.src + p.len == s && p.dstp + p.len == d) {
         p.len += len;
@@ -172,10 +176,17 @@ void proxy_main(epb_proxy* px, int tid, int nthreads) {
   const int C = ctx->cfg.fifo_channels;
   const int64_t cap = ctx->cfg.fifo_capacity, mask = cap - 1;
   std::vector<ChanState> chans;
+  // one stream per proxy thread: the thread's channels then execute in the
+  // order it serves them (stronger than required), and a rank needs only
+  // proxy_threads hardware queues — CUDA multiplexes streams onto
+  // CUDA_DEVICE_MAX_CONNECTIONS queues, and a proxy copy that lands in the
+  // queue of a kernel spinning on that very copy would wait for it forever
+  cudaStream_t st = nullptr;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   for (int ch = tid; ch < C; ch += nthreads) {
     ChanState cs;
     cs.ch = ch;
-    cudaStreamCreateWithFlags(&cs.st, cudaStreamNonBlocking);
+    cs.st = st;
     cudaHostAlloc(&cs.vals, sizeof(uint64_t) * kValueRing, cudaHostAllocDefault);
     cs.head = load_acquire(&ctx->fifo_host[ch][EPB_CTL_HEAD]);
     chans.push_back(cs);
@@ -227,13 +238,13 @@ void proxy_main(epb_proxy* px, int tid, int nthreads) {
       std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
   }
+  cudaStreamSynchronize(st);
   for (ChanState& cs : chans) {
-    cudaStreamSynchronize(cs.st);
     for (auto& pr : cs.inflight) cudaEventDestroy(pr.first);
     for (auto ev : cs.pool) cudaEventDestroy(ev);
-    cudaStreamDestroy(cs.st);
     cudaFreeHost(cs.vals);
   }
+  cudaStreamDestroy(st);
 }
 
 }  // namespace

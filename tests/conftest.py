@@ -8,6 +8,7 @@ ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 os.environ.setdefault("EPB_TIMEOUT_S", "20")
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # see paper_2512_19849_b200/__init__.py
 
 
 def pytest_configure(config):

@@ -44,7 +44,8 @@ def test_layout_parity(torch, R, T, E, k, mask):
     assert np.array_equal(in_rank.cpu().numpy(), o_in)
 
 
-def _emulated_dispatch(torch, R, Ts, H, E, k, seed, fp8=False, mask=0.0, zipf=0.0, num_sms=None, slots=3):
+def _emulated_dispatch(torch, R, Ts, H, E, k, seed, fp8=False, mask=0.0, zipf=0.0, num_sms=None, slots=3,
+                       ht="nvlink", grp=None):
     from paper_2512_19849_b200 import Config, LocalGroup
     g = np.random.default_rng(seed)
     xs, idxs, ws = [], [], []
@@ -54,7 +55,9 @@ def _emulated_dispatch(torch, R, Ts, H, E, k, seed, fp8=False, mask=0.0, zipf=0.
         idxs.append(idx)
         ws.append(w)
     from paper_2512_19849_b200 import nvl_bytes_hint
-    grp = LocalGroup(R, nvl_bytes_hint(max(Ts), H, R, k, slots), num_recv_slots=slots)
+    if grp is None:
+        grp = LocalGroup(R, nvl_bytes_hint(max(Ts), H, R, k, slots, ht_proxy=ht == "proxy"), num_recv_slots=slots,
+                         fifo_channels=4 if ht == "proxy" else 0, proxy_threads=2, ht_transport=ht)
     topk_dev, lay = _layout_dev(torch, grp, idxs, E)
     x_dev = [to_dev_bf16(x) for x in xs]
     scales = None
@@ -72,16 +75,28 @@ def _emulated_dispatch(torch, R, Ts, H, E, k, seed, fp8=False, mask=0.0, zipf=0.
     return grp, xs, idxs, ws, x_in, scales, lay, res
 
 
-@pytest.mark.parametrize("R,Ts,H,E,k,mask,sms", [
-    (1, [300], 1024, 16, 4, 0.0, None),
-    (2, [257, 64], 2048, 32, 4, 0.0, 7),
-    (4, [128, 128, 128, 128], 1024, 32, 2, 0.0, None),
-    (4, [0, 333, 1, 50], 7168, 64, 8, 0.2, 20),
-    (8, [200] * 8, 1024, 64, 8, 0.0, None),
+@pytest.mark.parametrize("R,Ts,H,E,k,mask,sms,ht", [
+    (1, [300], 1024, 16, 4, 0.0, None, "nvlink"),
+    (2, [257, 64], 2048, 32, 4, 0.0, 7, "nvlink"),
+    (4, [128, 128, 128, 128], 1024, 32, 2, 0.0, None, "nvlink"),
+    (4, [0, 333, 1, 50], 7168, 64, 8, 0.2, 20, "nvlink"),
+    (8, [200] * 8, 1024, 64, 8, 0.0, None, "nvlink"),
+    # the CPU-proxy data path (WRITE/ATOMIC TransferCmds)
+    (2, [257, 64], 2048, 32, 4, 0.0, 7, "proxy"),
+    (4, [0, 333, 1, 50], 7168, 64, 8, 0.2, 20, "proxy"),
+    (8, [200] * 8, 1024, 64, 8, 0.0, None, "proxy"),
 ])
-def test_dispatch_combine_emulated(torch, R, Ts, H, E, k, mask, sms):
-    grp, xs, idxs, ws, x_in, _, lay, res = _emulated_dispatch(torch, R, Ts, H, E, k, seed=R * 7 + H, mask=mask,
-                                                              num_sms=sms)
+def test_dispatch_combine_emulated(torch, R, Ts, H, E, k, mask, sms, ht):
+    grp = None
+    for it in range(2 if ht == "proxy" else 1):  # proxy: the signal counters must stay in step across calls
+        grp, xs, idxs, ws, x_in, _, lay, res = _emulated_dispatch(torch, R, Ts, H, E, k, seed=R * 7 + H + it,
+                                                                  mask=mask, num_sms=sms, ht=ht, grp=grp)
+        _check_dispatch_combine(torch, grp, R, E, xs, idxs, ws, res)
+    grp.check_device_error()
+    grp.destroy()
+
+
+def _check_dispatch_combine(torch, grp, R, E, xs, idxs, ws, res):
     in_ranks = [O.get_dispatch_layout(i, E, R)[2] for i in idxs]
     out, heads = O.dispatch(xs, in_ranks, idxs, ws, E)
     for d in range(R):
@@ -114,13 +129,12 @@ def test_dispatch_combine_emulated(torch, R, Ts, H, E, k, mask, sms):
         assert np.array_equal(got, ref[s][0]), s
         np.testing.assert_allclose(O.bf16_to_f32(got), O.bf16_to_f32(ref[s][0]), rtol=1e-2, atol=1e-3)
         assert comb[s][1] is None
-    grp.check_device_error()
-    grp.destroy()
 
 
-def test_dispatch_fp8_tuple_emulated(torch):
+@pytest.mark.parametrize("ht", ["nvlink", "proxy"])
+def test_dispatch_fp8_tuple_emulated(torch, ht):
     R, Ts, H, E, k = 4, [100, 90, 80, 70], 7168, 32, 8
-    grp, xs, idxs, ws, x_in, scales, lay, res = _emulated_dispatch(torch, R, Ts, H, E, k, seed=5, fp8=True)
+    grp, xs, idxs, ws, x_in, scales, lay, res = _emulated_dispatch(torch, R, Ts, H, E, k, seed=5, fp8=True, ht=ht)
     in_ranks = [O.get_dispatch_layout(i, E, R)[2] for i in idxs]
     qs = [u8_bits(q) for q, _ in x_in]
     out, _ = O.dispatch(qs, in_ranks, idxs, ws, E, x_scales=scales)

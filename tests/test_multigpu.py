@@ -46,29 +46,31 @@ def _worker(rank, world, port, results):
         Ts = [700 + 97 * r for r in range(R)]
         H, E, k = 7168, 64, 8
         xs, idxs, ws = _inputs(R, Ts, H, E, k, seed=1)
-        buf = epb.Buffer(dist.group.WORLD, epb.nvl_bytes_hint(max(Ts), H, R, k), 0)
         topk = torch.from_numpy(idxs[rank]).cuda()
         w = torch.from_numpy(ws[rank]).cuda()
-        for it in range(3):  # repeat: exercises both parities / epochs and slot reuse
-            per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(topk, E)
-            recv_x, rti, rtw, lst, handle, _ = buf.dispatch(
-                to_dev_bf16(xs[rank]), num_tokens_per_rank=per_rank, is_token_in_rank=in_rank,
-                num_tokens_per_expert=per_exp, topk_idx=topk, topk_weights=w)
-            in_ranks = [O.get_dispatch_layout(i, E, R)[2] for i in idxs]
-            out, heads = O.dispatch(xs, in_ranks, idxs, ws, E)
-            o = out[rank]
-            assert np.array_equal(bf16_bits(recv_x), o["recv_x"]), "recv_x"
-            assert np.array_equal(rti.cpu().numpy(), o["recv_topk_idx"]), "recv_topk_idx"
-            assert np.array_equal(rtw.cpu().numpy(), o["recv_topk_weights"]), "recv_topk_weights"
-            assert lst == o["num_recv_per_expert"], "per expert"
-            g = np.random.default_rng(50 + it)
-            ys = [bf16_random(g, oo["recv_x"].shape) for oo in out]
-            comb, comb_w, _ = buf.combine(to_dev_bf16(ys[rank]), handle, topk_weights=rtw)
-            ref = O.combine(ys, in_ranks, heads, out[0]["rank_prefix_matrix"],
-                            [oo["recv_topk_weights"] for oo in out])
-            assert np.array_equal(bf16_bits(comb), ref[rank][0]), "combine"
-            assert np.array_equal(comb_w.cpu().numpy(), ref[rank][1]), "combine weights"
-        buf.destroy()
+        for ht in ("nvlink", "proxy"):  # kernels' NVLink stores / the CPU proxy's WRITE+ATOMIC commands
+            buf = epb.Buffer(dist.group.WORLD, epb.nvl_bytes_hint(max(Ts), H, R, k, ht_proxy=ht == "proxy"), 0,
+                             fifo_channels=4, ht_transport=ht)
+            for it in range(3):  # repeat: exercises both parities / epochs and slot reuse
+                per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(topk, E)
+                recv_x, rti, rtw, lst, handle, _ = buf.dispatch(
+                    to_dev_bf16(xs[rank]), num_tokens_per_rank=per_rank, is_token_in_rank=in_rank,
+                    num_tokens_per_expert=per_exp, topk_idx=topk, topk_weights=w)
+                in_ranks = [O.get_dispatch_layout(i, E, R)[2] for i in idxs]
+                out, heads = O.dispatch(xs, in_ranks, idxs, ws, E)
+                o = out[rank]
+                assert np.array_equal(bf16_bits(recv_x), o["recv_x"]), "recv_x"
+                assert np.array_equal(rti.cpu().numpy(), o["recv_topk_idx"]), "recv_topk_idx"
+                assert np.array_equal(rtw.cpu().numpy(), o["recv_topk_weights"]), "recv_topk_weights"
+                assert lst == o["num_recv_per_expert"], "per expert"
+                g = np.random.default_rng(50 + it)
+                ys = [bf16_random(g, oo["recv_x"].shape) for oo in out]
+                comb, comb_w, _ = buf.combine(to_dev_bf16(ys[rank]), handle, topk_weights=rtw)
+                ref = O.combine(ys, in_ranks, heads, out[0]["rank_prefix_matrix"],
+                                [oo["recv_topk_weights"] for oo in out])
+                assert np.array_equal(bf16_bits(comb), ref[rank][0]), "combine"
+                assert np.array_equal(comb_w.cpu().numpy(), ref[rank][1]), "combine weights"
+            buf.destroy()
         # ---- low latency, both transports ------------------------------------------
         Tm, H2, E2, k2 = 128, 7168, 32 * R, 8
         xs2, idx2, w2 = _inputs(R, Tm, H2, E2, k2, seed=2)
