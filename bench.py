@@ -358,7 +358,13 @@ def run_ours(args):
         for name, kw in (("dsv3_fp8_dispatch", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, fp8=True, buf=buf)),
                          ("dsv3_bf16_combine_push", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, combine_in_region=False,
                                                          buf=buf)),
-                         ("qwen3_235b_zipf", dict(T=8192, H=4096, E=128, zipf=1.0))):
+                         ("qwen3_235b_zipf", dict(T=8192, H=4096, E=128, zipf=1.0)),
+                         ("dsv3_bf16_ht_proxy", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, ht="proxy"))):
+            # the proxy HT transport is opt-in here (its first call can
+            # stall when another Buffer of the process has run a combine)
+            only = os.environ.get("EPB_BENCH_CONFIGS")
+            if (only and name not in only.split(",")) or (not only and kw.get("ht") == "proxy"):
+                continue
             try:
                 configs[name] = config_bench(name, *common, **kw)
             except Exception as exc:
@@ -395,7 +401,7 @@ def run_ours(args):
 
 
 def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T, H, E, fp8=False, zipf=0.0,
-                 combine_in_region=True, buf=None):
+                 combine_in_region=True, buf=None, ht="nvlink"):
     """Per-op device times of the other BASELINE.json normal-mode rows
     (SURVEY.md §8(d)): FP8 dispatch of DS-V3, Qwen3-235B with Zipf routing,
     and combine on expert outputs allocated OUTSIDE the arena (push mode).
@@ -406,7 +412,8 @@ def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T,
     from tests.helpers import bf16_random, make_routing
     own = buf is None
     if own:
-        buf = epb.Buffer(group, epb.nvl_bytes_hint(T, H, R, TOPK, 2), 0, num_recv_slots=2)
+        buf = epb.Buffer(group, epb.nvl_bytes_hint(T, H, R, TOPK, 2, ht_proxy=ht == "proxy"), 0, num_recv_slots=2,
+                         fifo_channels=8 if ht == "proxy" else 0, proxy_threads=4, ht_transport=ht)
     g = np.random.default_rng(31_000 + 97 * rank + int(zipf * 10))
     idx, w = make_routing(g, T, E, TOPK, zipf=zipf)
     x = torch.from_numpy(bf16_random(g, (T, H)).view(np.int16)).view(torch.bfloat16).to(dev)
@@ -420,6 +427,44 @@ def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T,
     remote = int(m.sum())
     reps = max(10, min(args.steps, 30))
     d_ms, c_ms = [], []
+    try:
+        return _config_loop(buf, own, idx_t, w_t, x_in, fp8, combine_in_region, flush, remote, reps, T, H, E, zipf, ht,
+                            row_bytes, R, dev, barrier, max_over_ranks, d_ms, c_ms)
+    except Exception:
+        if ht == "proxy":
+            _proxy_diag(buf, rank)
+        raise
+
+
+def _proxy_diag(buf, rank):
+    """stderr dump of the proxy state of one rank (FIFO ctl words, counters)."""
+    import ctypes as C
+    import torch
+    from paper_2512_19849_b200._lib import lib
+    from paper_2512_19849_b200.buffer import _SlotMemory
+    rk = buf._rank
+    st = (C.c_int64 * 3)()
+    lib.epb_proxy_stats(rk.ctx, st)
+    ctl = []
+    for ch in range(rk.cfg.fifo_channels):
+        q, cap = C.POINTER(C.c_int64)(), C.c_int64()
+        lib.epb_fifo_ctl(rk.ctx, ch, C.byref(q), C.byref(cap))
+        ctl.append((q[0], q[8], q[16]))
+        if q[0]:
+            from paper_2512_19849_b200 import command as cmdmod
+            for i in range(q[0]):
+                lo, hi = q[32 + 2 * i] & (2**64 - 1), q[33 + 2 * i] & (2**64 - 1)
+                c = cmdmod.unpack(lo, hi)
+                print(f"   ch{ch} #{i}: kind={c.kind} dst={c.dst_rank} so={c.src_offset} do={c.dst_offset} "
+                      f"len={c.length_or_value} flags={c.flags}", file=sys.stderr, flush=True)
+    sig = torch.as_tensor(_SlotMemory(rk.base + 4416, 128), device=rk.device).view(torch.int64).cpu().tolist()
+    print(f"[proxy diag rank {rank}] served/copies/atomics {list(st)} ctl(tail,head,completed) {ctl} "
+          f"ht_sig {sig[:8]} | {sig[8:]}", file=sys.stderr, flush=True)
+
+
+def _config_loop(buf, own, idx_t, w_t, x_in, fp8, combine_in_region, flush, remote, reps, T, H, E, zipf, ht,
+                 row_bytes, R, dev, barrier, max_over_ranks, d_ms, c_ms):
+    import torch
     for it in range(reps + 3):
         per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(idx_t, E)
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -449,8 +494,10 @@ def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T,
     rem_max = max_over_ranks(float(remote))
     d, c = statistics.median(d_ms), statistics.median(c_ms)
     out = {"tokens_per_rank": T, "hidden": H, "experts": E, "topk": TOPK, "dispatch_dtype": "fp8" if fp8 else "bf16",
-           "routing": f"zipf({zipf})" if zipf else "uniform", "dispatch_us": round(d * 1e3, 2),
-           "combine_us": round(c * 1e3, 2), "combine_input": "arena view (pull)" if y_in_region(fp8, combine_in_region)
+           "routing": f"zipf({zipf})" if zipf else "uniform", "transport": "CPU proxy (FIFO + copy engine)"
+           if ht == "proxy" else "SM stores/loads over NVLink", "dispatch_us": round(d * 1e3, 2),
+           "combine_us": round(c * 1e3, 2), "combine_input": ("arena view (WRITE in place)" if ht == "proxy" else "arena view (pull)")
+           if y_in_region(fp8, combine_in_region)
            else "device tensor outside the arena (push)", "reps": reps}
     if R > 1:
         out["max_remote_rows"] = int(rem_max)

@@ -6,6 +6,7 @@
 // kernels can store straight into peer memory over NVLink.
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -173,6 +174,13 @@ extern "C" int epb_open_peers(epb_t* ctx, const void* handles) {
                                                                          cudaGetErrorString(e));
     ctx->peer[r] = static_cast<char*>(p);
     ctx->peer_ipc[r] = true;
+    // touch the mapping with a copy now (read and write): the first copy-engine
+    // access to a lazily enabled peer mapping can stall for ~100 ms, which must
+    // not happen while a kernel spins on a proxy copy's completion
+    const size_t probe = offsetof(epb::Scratch, trace) + epb::kMetaBytes;  // scratch words nobody reads remotely
+    e = cudaMemcpy(ctx->base + probe, ctx->peer[r] + probe, 16, cudaMemcpyDefault);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->peer[r] + probe + 16, ctx->base + probe + 16, 16, cudaMemcpyDefault);
+    if (e != cudaSuccess) return epb_cuda_check(e, "peer mapping warm-up copy");
   }
   if (!ctx->barrier) {  // the proxies' all-peer barrier segment, named after the job's handles
     const std::string name = epb_barrier_name(handles, (size_t)ctx->world * EPB_IPC_HANDLE_BYTES);

@@ -515,12 +515,20 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
       const uint32_t old = atom_add_acq_rel_gpu(&meta_of(rv.base)->disp_done[me], 1u);
       if (old + 1 == P.target[lr]) push_dispatch_cmds(P, lr, s_slotv, s_base, s_mine, s_pre, s_abort != 0);
     }
-    if (c == 0 && tid < R) {
-      if (tid == me) wait_geq(rv, &meta_of(rv.base)->disp_done[me], P.target[lr], 0x200 + tid);
-      else wait_geq64(rv, &meta_of(rv.base)->ht_sig[0][tid], P.ht_calls[lr], 0x220 + tid, 500);
-    }
+    // the peers' rows are awaited by dispatch_proxy_wait_kernel, launched next
+    // on the stream: no block of this kernel stays resident spinning on copies
+    // the proxy issues (a copy-engine transfer was observed to stall behind one)
   }
   trace_mark(rv, 10);
+}
+
+// Proxy transport: one block per local rank waits until every peer's rows
+// (and its ATOMIC) have landed; my own rows were written by the kernel above.
+__global__ void dispatch_proxy_wait_kernel(const __grid_constant__ DispatchParams P) {
+  const RankView& rv = P.rv[blockIdx.x];
+  const int tid = threadIdx.x;
+  if (tid < rv.world && tid != rv.rank)
+    wait_geq64(rv, &meta_of(rv.base)->ht_sig[0][tid], P.ht_calls[blockIdx.x], 0x220 + tid, 500);
 }
 
 }  // namespace epb
@@ -574,6 +582,10 @@ extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_
   void* kargs[] = {&P};
   EPB_CUDA(epb_launch_grid_sync((void*)dispatch_kernel, dim3(num_channels, n_local), dim3(kDispatchThreads),
                                        kargs, smem, st));
+  if (P.proxy) {
+    dispatch_proxy_wait_kernel<<<n_local, 32, 0, st>>>(P);
+    EPB_CUDA(cudaGetLastError());
+  }
   return EPB_OK;
 }
 
