@@ -421,8 +421,12 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   trace_mark_max(rv, 20);
   if (pull) {
     __syncthreads();  // this block's reads of the peers' inputs are complete
-    if (tid < R) bump_done(rv, tid, me);
-    if (b == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
+    if (R == 1) {     // no peer reads my input: only keep the counter in step
+      if (tid == 0) atomicAdd(&meta_of(rv.base)->comb_done[0], 1u);
+    } else {
+      if (tid < R) bump_done(rv, tid, me);
+      if (b == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
+    }
   }
 }
 
