@@ -347,7 +347,9 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
     }
     return;
   }
-  if (b == 0 && tid < R) {  // my offsets to every peer: tagged words (16-byte / 4-byte units)
+  if (R == 1) {  // single rank: my own input is read in place in either mode
+    if (tid == 0) s_xoff[0] = 0;
+  } else if (b == 0 && tid < R) {  // my offsets to every peer: tagged words (16-byte / 4-byte units)
     const char* xp = static_cast<const char*>(a.x);
     const char* wp = reinterpret_cast<const char*>(a.topk_weights);
     const char* lo = rv.base;
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
     st_relaxed_sys(&m[0], tagged(xo, epoch));
     st_relaxed_sys(&m[1], tagged(wo, epoch));
   }
-  if (tid < 2 * R) {
+  if (tid < 2 * R && R > 1) {
     const int s = tid >> 1, f = tid & 1;
     const uint32_t v = wait_tagged(rv, &meta_of(rv.base)->comb_msg[par][s][f], epoch, 0x380 + s);
     const int64_t off = v == kNotifyAbort ? -1 : (int64_t)v * (f ? 4 : 16);

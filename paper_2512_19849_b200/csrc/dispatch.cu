@@ -207,7 +207,16 @@ __device__ __forceinline__ void exchange_counts(const DispatchParams& P, int lr,
   }
   __syncthreads();
   trace_mark(rv, 1);
-  if (warp < R) {
+  if (R == 1 && warp == 0) {
+    // single rank: no mailbox round trip — my totals and slot are the plan's inputs
+    int s = 0;
+    for (int cc = lane; cc < C; cc += 32) s += s_cnt[0][cc];
+    s = __reduce_add_sync(0xffffffffu, s);
+    if (lane == 0) {
+      s_rpm[0][0] = s;
+      s_slot[0] = a.recv_slot;
+    }
+  } else if (warp < R) {
     // what peer d's plan needs: my per-rank totals and my receive slot
     const int d = warp;
     NotifyMsg* msg = &meta_of(rv.peer[d])->mbox[par][me];
@@ -247,13 +256,13 @@ __device__ __forceinline__ void exchange_counts(const DispatchParams& P, int lr,
   constexpr int kPer = (kMaxRanks * (kMaxRanks + 1) + 31) / 32;
   uint64_t v[kPer];
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
+  for (int j = 0; j < kPer && R > 1; ++j) {
     const int i = lane + 32 * j, s = i / (R + 1), f = i % (R + 1);
     v[j] = i < R * (R + 1) ? ld_relaxed_sys(f < R ? &my->mbox[par][s].counts_per_rank[f] : &my->mbox[par][s].slot)
                            : tagged(0, epoch);
   }
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
+  for (int j = 0; j < kPer && R > 1; ++j) {
     const int i = lane + 32 * j, s = i / (R + 1), f = i % (R + 1);
     if (i < R * (R + 1)) {
       const uint64_t* w = f < R ? &my->mbox[par][s].counts_per_rank[f] : &my->mbox[par][s].slot;
