@@ -87,6 +87,9 @@ int epb_clear_device_error(epb_t* ctx);
 int epb_num_sms(void);
 /* Phase timestamps (64 x %globaltimer ns) recorded by the kernels when EPB_TRACE=1. */
 int epb_trace(epb_t* ctx, int64_t* out64);
+/* Diagnostics: one thread writes %globaltimer (ns) to the device word *dst, in
+   stream order (brackets launches on the same clock as epb_trace's marks). */
+int epb_debug_stamp(int64_t* dst, void* stream);
 /* Base device address of this rank's symmetric region and its size. */
 int epb_region(epb_t* ctx, void** base, size_t* bytes);
 

@@ -118,3 +118,12 @@ extern "C" int epb_fifo_device_bench(epb_t* ctx, int64_t num_cmds, int channels,
   if (ctx->host->err_code) return epb_set_error((int)ctx->host->err_code, "device FIFO bench reported an error");
   return EPB_OK;
 }
+
+namespace epb {
+__global__ void stamp_kernel(int64_t* dst) { *dst = (int64_t)globaltimer(); }
+}  // namespace epb
+
+extern "C" int epb_debug_stamp(int64_t* dst, void* stream) {
+  epb::stamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(dst);
+  return epb_cuda_check(cudaGetLastError(), "stamp");
+}

@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
         a.recv_route[(int64_t)le * RT + j] = (int32_t)(s * g.rows_per_src + row);
       }
     }
+    trace_mark_max(rv, 29);
   }
 }
 
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
   const int RT = R * g.Tmax;
   const int n16 = H / 8;
   __shared__ int32_t s_tot[kMaxLocalExperts + 1];
+  trace_mark(rv, 32);
 
   if (sending) {
     for (int le = tid; le < L; le += blockDim.x) s_tot[le + 1] = a.packed_recv_count[le];
@@ -462,6 +464,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
         st_na_v4(out + i1, make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]));
       }
     }
+    trace_mark_max(rv, 35);
   }
 }
 
