@@ -657,6 +657,9 @@ def main():
     ap.add_argument("--no-ll", action="store_true", help="skip the low-latency sub-benchmarks (e.g. under ncu)")
     ap.add_argument("--no-configs", action="store_true", help="skip the FP8 / push-combine / Qwen3 sub-benchmarks")
     args = ap.parse_args()
+    if os.environ.get("EPB_BENCH_WATCHDOG"):  # debugging: dump every thread's stack and exit after N s
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["EPB_BENCH_WATCHDOG"]), exit=True)
     if args.impl == "reference":
         run_reference(args)
     else:

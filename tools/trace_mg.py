@@ -32,7 +32,7 @@ y = torch.randn(E // world, world * 128, H, device="cuda").to(torch.bfloat16)
 NAMES = {2: "gather start", 0: "start", 1: "arrive+counts", 3: "post msgs", 4: "peers' msgs", 5: "plan published",
          6: "host publish", 7: "plan loaded", 9: "copies done", 10: "all arrived", 15: "combine entry", 16: "combine start",
          17: "push done", 18: "barrier", 19: "reduce done", 24: "ll_disp start", 25: "bitmap", 26: "items done",
-         27: "ticket", 28: "recv wait", 29: "ll_disp last block done", 32: "ll_comb start", 33: "ll_comb items", 34: "ll_comb wait", 35: "ll_comb last block done", 11: "last block copy start", 12: "last block copies done", 20: "last block reduce done", 21: "last block reduce start"}
+         27: "ticket", 28: "recv wait", 29: "ll_disp last block done", 32: "ll_comb start", 33: "ll_comb items", 34: "ll_comb wait", 35: "ll_comb last block done", 22: "consumers done (max)", **{40 + w: f"wave{w} ready" for w in range(8)}, **{48 + w: f"wave{w} pushed(b0)" for w in range(8)}, 11: "last block copy start", 12: "last block copies done", 20: "last block reduce done", 21: "last block reduce start"}
 
 
 def snap():
@@ -45,10 +45,10 @@ def show(label, snaps):
     """Median over calls of each mark's offset from the first mark of its group."""
     import statistics
     print(label, flush=True)
-    for a, b in [(0, 12), (15, 21), (24, 29), (32, 35)]:
+    for grp in [range(0, 13), list(range(15, 23)) + list(range(40, 56)), range(24, 30), range(32, 36)]:
         offs = {}
         for ts in snaps:
-            keys = [k for k in sorted(ts) if a <= k <= b]
+            keys = [k for k in sorted(ts) if k in grp]
             if not keys:
                 continue
             for k in keys:
