@@ -53,8 +53,10 @@ struct NotifyMsg {                          // one source rank's dispatch counts
 struct Meta {
   uint32_t disp_done[kMaxRanks];         // += 1 per dispatch block of src (monotonic)
   uint32_t comb_done[kMaxRanks];         // += 1 per combine block of src (monotonic)
-  uint64_t ll_disp_flag[2][kMaxRanks];   // LL dispatch: epoch stamp per src
-  uint64_t ll_comb_flag[2][kMaxRanks];   // LL combine: epoch stamp per src
+  // LL direct transport: += 1 per sender block of src once its rows (and, for
+  // block 0, the count header) have landed; the receiver resets after use
+  uint32_t ll_disp_cnt[2][kMaxRanks];
+  uint32_t ll_comb_cnt[2][kMaxRanks];
   uint64_t proxy_sig[kMaxFifo][kMaxRanks];  // CPU-proxy signals: += 1 per piggybacked WRITE from src on channel
   uint64_t ht_sig[2][kMaxRanks];         // proxy HT transport: src's ATOMIC += 1 per [dispatch|combine] call
   // combine mode message (tagged words): where src's input rows / weights live

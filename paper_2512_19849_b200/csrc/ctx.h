@@ -27,6 +27,7 @@ struct epb_ctx {
   int num_sms = 148;
   uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;
   int trace = 0;                        // EPB_TRACE=1: kernels record phase timestamps
+  int ll_grid[2] = {0, 0};              // LL dispatch / combine grid width, pinned at the first call
   // LL bookkeeping of the last dispatch (shape) for combine validation.
   int ll_last_tokens = -1;
   // GPU -> CPU command FIFOs (pinned, mapped) and the proxy.

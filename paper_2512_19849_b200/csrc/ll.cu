@@ -196,35 +196,50 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       if (ch == 0 && p != 0) *reinterpret_cast<int32_t*>(reinterpret_cast<char*>(p) + meta_off) = t;
     }
 
-    // the last block of this rank publishes the per-expert counts and the signal
     __shared__ uint32_t s_last;
     __syncthreads();
     trace_mark(rv, 26);
+    if (!P.use_proxy) {
+      // direct transport: every block signals every destination itself once its
+      // rows are stored (release cumulativity over the block barrier); block 0
+      // first writes each destination's per-expert count header.  No ticket,
+      // no system fence on the receiver's critical path.
+      if (blockIdx.x == 0) {
+        for (int i = tid; i < R * L; i += blockDim.x) {
+          const int d = i / L, le = i % L;
+          char* blk = rv.peer[d] + P.ll_off + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
+          reinterpret_cast<int32_t*>(blk)[le] = cnt[i];
+        }
+        __syncthreads();
+      }
+      if (tid < R) red_release_sys_add(&meta_of(rv.peer[tid])->ll_disp_cnt[par][me], 1u);
+    }
+    // the ticket only tracks the device-resident epoch (and, for the proxy
+    // transport, hands the rows to the FIFO): the last block bumps it
     if (tid == 0) s_last = atom_add_acq_rel_gpu(&sc->ll_ticket[par], 1u) == gridDim.x - 1;
     __syncthreads();
     trace_mark(rv, 27);
     if (s_last && warp == 0) {
-      for (int d = 0; d < R; ++d) {
-        char* blk = P.use_proxy ? my_ll + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block
-                                : rv.peer[d] + P.ll_off + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
-        for (int le = lane; le < L; le += 32) reinterpret_cast<int32_t*>(blk)[le] = cnt[d * L + le];
-      }
-      fence_sys();
-      __syncwarp();
-      if (!P.use_proxy) {
-        if (lane < R) st_release_sys(&meta_of(rv.peer[lane])->ll_disp_flag[par][me], (uint64_t)epoch);
-      } else if (lane == 0) {
+      if (P.use_proxy) {
         for (int d = 0; d < R; ++d) {
-          int rows = 0;
-          for (int le = 0; le < L; ++le) rows += cnt[d * L + le];
-          const int ch = d % P.disp_channels;
-          const int64_t rel = P.ll_off - (int64_t)kRegionHeader;  // commands address the arena start
-          const int64_t src_off = rel + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
-          const int64_t dst_off = rel + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
-          const int64_t len = g.hdr_bytes + (int64_t)rows * rstride;
-          uint64_t lo, hi;
-          cmd_pack_dev(EPB_CMD_WRITE, d, ch, src_off, dst_off, len, EPB_FLAG_PIGGYBACK_ATOMIC, lo, hi);
-          fifo_push(rv, ch, lo, hi);
+          char* blk = my_ll + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
+          for (int le = lane; le < L; le += 32) reinterpret_cast<int32_t*>(blk)[le] = cnt[d * L + le];
+        }
+        fence_sys();
+        __syncwarp();
+        if (lane == 0) {
+          for (int d = 0; d < R; ++d) {
+            int rows = 0;
+            for (int le = 0; le < L; ++le) rows += cnt[d * L + le];
+            const int ch = d % P.disp_channels;
+            const int64_t rel = P.ll_off - (int64_t)kRegionHeader;  // commands address the arena start
+            const int64_t src_off = rel + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
+            const int64_t dst_off = rel + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
+            const int64_t len = g.hdr_bytes + (int64_t)rows * rstride;
+            uint64_t lo, hi;
+            cmd_pack_dev(EPB_CMD_WRITE, d, ch, src_off, dst_off, len, EPB_FLAG_PIGGYBACK_ATOMIC, lo, hi);
+            fifo_push(rv, ch, lo, hi);
+          }
         }
       }
       if (lane == 0) {
@@ -242,7 +257,9 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     int32_t* s_pre = s_off + R * L;                       // [R][L] prefix over experts (row in block)
     int32_t* s_tot = s_pre + R * L;                       // [L + 1] prefix over experts of totals
     if (tid < R) {
-      if (!P.use_proxy) wait_geq64(rv, &my_meta->ll_disp_flag[par][tid], (uint64_t)epoch, 0x600 + tid);
+      // cumulative: every call of this parity adds gridDim.x per source (the
+      // grid width is pinned per context, epb_ll_dispatch)
+      if (!P.use_proxy) wait_geq(rv, &my_meta->ll_disp_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x600 + tid);
       else wait_geq64(rv, &my_meta->proxy_sig[me % P.disp_channels][tid], pexp, 0x680 + tid);
     }
     __syncthreads();
@@ -362,12 +379,11 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
     __shared__ uint32_t s_last;
     __syncthreads();
     trace_mark(rv, 33);
+    if (!P.use_proxy && tid < R) red_release_sys_add(&meta_of(rv.peer[tid])->ll_comb_cnt[par][me], 1u);
     if (tid == 0) s_last = atom_add_acq_rel_gpu(&sc->ll_ticket[2 + par], 1u) == gridDim.x - 1;
     __syncthreads();
     if (s_last && warp == 0) {
-      if (!P.use_proxy) {
-        if (lane < R) st_release_sys(&meta_of(rv.peer[lane])->ll_comb_flag[par][me], (uint64_t)epoch);
-      } else if (lane == 0) {
+      if (P.use_proxy && lane == 0) {
         for (int s = 0; s < R; ++s) {
           int64_t rows = 0;
           for (int le = 0; le < L; ++le) rows += a.packed_recv_layout_range[le * R + s] & 0xffffffffll;
@@ -390,7 +406,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
 
   if (P.phases & 2) {
     if (tid < R) {
-      if (!P.use_proxy) wait_geq64(rv, &my_meta->ll_comb_flag[par][tid], (uint64_t)epoch, 0x700 + tid);
+      if (!P.use_proxy) wait_geq(rv, &my_meta->ll_comb_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x700 + tid);
       else wait_geq64(rv, &my_meta->proxy_sig[P.disp_channels + me % P.disp_channels][tid], pexp, 0x780 + tid);
     }
     __syncthreads();
@@ -510,10 +526,17 @@ static int check_group_ll(epb_t* const* ctxs, int n) {
   return EPB_OK;
 }
 
-static int ll_blocks(epb_t* const* ctxs, int n_local, int num_sms, const void* kernel, size_t smem) {
+// The direct transport's completion counters are cumulative per source (each
+// call adds one per sender block), so a context keeps the grid width of its
+// first call of each kind; every rank derives the same width from the same
+// num_sms.  Returns 0 if that width can no longer be co-resident.
+static int ll_blocks(epb_t* const* ctxs, int n_local, int num_sms, const void* kernel, size_t smem, int kind) {
   const int max_active = std::max(1, epb_max_active_blocks(kernel, kLLThreads, smem));
-  int nb = std::max(1, num_sms / n_local);
-  return std::min(nb, std::max(1, max_active * ctxs[0]->num_sms / n_local));
+  const int cap = std::max(1, max_active * ctxs[0]->num_sms / n_local);
+  int& pinned = ctxs[0]->ll_grid[kind];
+  if (pinned == 0) pinned = std::min(std::max(1, num_sms / n_local), cap);
+  for (int i = 1; i < n_local; ++i) ctxs[i]->ll_grid[kind] = pinned;
+  return pinned <= cap ? pinned : 0;
 }
 
 static int ll_transport(epb_ctx* c, int use_proxy, int* disp_channels) {
@@ -553,7 +576,8 @@ extern "C" int epb_ll_dispatch(epb_t* const* ctxs, int n_local, const epb_ll_dis
   const size_t smem = std::max(smem_send, smem_recv);
   if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "LL dispatch shape needs too much shared memory");
   EPB_CUDA(epb_ensure_smem((const void*)ll_dispatch_kernel, smem));
-  const int nb = ll_blocks(ctxs, n_local, num_sms, (const void*)ll_dispatch_kernel, smem);
+  const int nb = ll_blocks(ctxs, n_local, num_sms, (const void*)ll_dispatch_kernel, smem, 0);
+  if (nb == 0) return epb_set_error(EPB_ERR_CONFIG, "LL dispatch: this shape no longer fits the context's pinned grid");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* kargs[] = {&P};
   EPB_CUDA(epb_launch_grid_sync((void*)ll_dispatch_kernel, dim3(nb, n_local), dim3(kLLThreads), kargs, smem, st));
@@ -580,7 +604,8 @@ extern "C" int epb_ll_combine(epb_t* const* ctxs, int n_local, const epb_ll_comb
     P.rv[i] = c->view();
     P.a[i] = args[i];
   }
-  const int nb = ll_blocks(ctxs, n_local, num_sms, (const void*)ll_combine_kernel, 0);
+  const int nb = ll_blocks(ctxs, n_local, num_sms, (const void*)ll_combine_kernel, 0, 1);
+  if (nb == 0) return epb_set_error(EPB_ERR_CONFIG, "LL combine: grid no longer co-resident");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* kargs[] = {&P};
   EPB_CUDA(epb_launch_grid_sync((void*)ll_combine_kernel, dim3(nb, n_local), dim3(kLLThreads), kargs, 0, st));
