@@ -67,10 +67,14 @@ typedef struct {
   int fifo_channels;    /* GPU->CPU command FIFOs (0 = no proxy)            */
   int fifo_capacity;    /* kMaxInflight per FIFO, power of two */
   int proxy_threads;    /* CPU proxy threads (PAPER.md:469 uses 4)          */
-  int ht_transport;     /* normal mode data path: 0 = NVLink stores from the
-                           kernels, 1 = CPU proxy (WRITE/ATOMIC TransferCmds;
-                           the arena then also holds one send-staging slot)  */
+  int ht_transport;     /* normal mode data path (EPB_HT_*): NVLink stores from
+                           the kernels into worst-case receive slots; the CPU
+                           proxy (WRITE/ATOMIC TransferCmds; the arena then also
+                           holds one send-staging slot); or bounded chunked
+                           ring channels (the arena holds only the rings)    */
 } epb_config_t;
+
+enum { EPB_HT_NVLINK = 0, EPB_HT_PROXY = 1, EPB_HT_RING = 2 };
 
 int epb_create(epb_t** out, int rank, int world, const epb_config_t* cfg);
 int epb_destroy(epb_t* ctx);
@@ -161,6 +165,72 @@ typedef struct {
 } epb_combine_args_t;
 
 int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_args_t* args, int num_sms, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Chunked ring channels (SPEC.md:409-413 RingChannel,        */
+/* :436-444 dispatch_ht; imm.py:28-31 HT_ROLE_HEAD credit   */
+/* return).  ht_transport = EPB_HT_RING: the arena holds only bounded rings,   */
+/* one per (source rank, lane) at every receiver for the dispatch and one per  */
+/* (expert rank, lane) at every source for the combine; the receive tensors    */
+/* are ordinary device memory sized from the notified counts.  A sender        */
+/* writes 32-token chunks into the ring slots tail..tail+n,      */
+/* then release-stores the tail; the receiver copies (dispatch) or reduces      */
+/* (combine) them and release-stores the head back at the sender (credit).     */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int lanes;              /* ring lanes (sender + receiver block pair each)      */
+  int ring_tokens;        /* slots per ring, a multiple of the 32-token chunk     */
+  int64_t disp_slot_bytes, comb_slot_bytes;
+  int64_t disp_off, comb_off;  /* ring areas inside the region                  */
+  int64_t bytes_needed;
+} epb_ring_layout_t;
+
+/* Ring geometry for rows of `hidden` (bf16 sized) and num_topk; lanes <= 0
+   picks the default for n_local ranks per GPU. */
+int epb_ring_layout(epb_t* ctx, int hidden, int num_topk, int lanes, int n_local, epb_ring_layout_t* out);
+
+/* The count exchange of epb_dispatch alone: fills the handle outputs
+   (rank/channel prefix matrices, send_head) and publishes the host counts
+   (epb_wait_notify); no rows move and no receive-slot capacity applies. */
+int epb_dispatch_notify(epb_t* const* ctxs, int n_local, const epb_dispatch_args_t* args, int num_channels,
+                        void* stream);
+
+typedef struct {
+  const void* x;              /* [T, hidden] bf16 (elem_bytes 2) or e4m3 (1)   */
+  const float* x_scales;      /* [T, num_scales] or NULL                       */
+  int hidden, elem_bytes, num_scales;
+  const int64_t* topk_idx;    /* [T, num_topk] or NULL                         */
+  const float* topk_weights;  /* [T, num_topk] or NULL                         */
+  int num_topk, num_tokens, num_experts;
+  const int32_t* rank_prefix_matrix;          /* from epb_dispatch_notify       */
+  const int32_t* recv_channel_prefix_matrix;
+  const int32_t* send_head;
+  int num_channels;                           /* C of epb_dispatch_notify       */
+  void* recv_x;               /* [N_recv, hidden] (device memory of the caller) */
+  float* recv_x_scales;       /* [N_recv, num_scales] or NULL                  */
+  int64_t* recv_topk_idx;     /* [N_recv, num_topk] or NULL                    */
+  float* recv_topk_weights;   /* [N_recv, num_topk] or NULL                    */
+  int32_t* recv_src_idx;      /* [N_recv]                                      */
+} epb_ring_dispatch_args_t;
+
+int epb_ring_dispatch(epb_t* const* ctxs, int n_local, const epb_ring_dispatch_args_t* args, int lanes,
+                      void* stream);
+
+typedef struct {
+  const void* x;              /* [N_recv, hidden] bf16 expert outputs, my receive order */
+  const float* topk_weights;  /* [N_recv, num_topk] or NULL                    */
+  int num_recv, hidden, num_topk;
+  const int32_t* rank_prefix_matrix;
+  const int32_t* recv_channel_prefix_matrix;
+  const int32_t* send_head;
+  int num_channels;
+  int num_tokens;
+  void* combined_x;              /* [T, hidden] bf16                            */
+  float* combined_topk_weights;  /* [T, num_topk] or NULL                       */
+} epb_ring_combine_args_t;
+
+int epb_ring_combine(epb_t* const* ctxs, int n_local, const epb_ring_combine_args_t* args, int lanes,
+                     void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Low-latency mode  (DeepEP low_latency_dispatch/combine)  */

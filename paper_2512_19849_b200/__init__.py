@@ -20,11 +20,11 @@ import os as _os
 _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 from . import _lib  # noqa: F401,E402  (loads libepb200.so or raises)
-from .buffer import Buffer, Config, EventOverlap, LocalGroup, nvl_bytes_hint
+from .buffer import Buffer, Config, EventOverlap, LocalGroup, nvl_bytes_hint, ring_nvl_bytes
 from .errors import (ChannelShutdown, ConfigError, ConnectionError_, EpsimError, FaultError, InvariantViolation,
                      ProtocolViolation, RingDeadlock, UnsupportedOperation)
 from .ops import per_token_cast_to_fp8
 
-__all__ = ["Buffer", "Config", "EventOverlap", "LocalGroup", "nvl_bytes_hint", "per_token_cast_to_fp8",
+__all__ = ["Buffer", "Config", "EventOverlap", "LocalGroup", "nvl_bytes_hint", "ring_nvl_bytes", "per_token_cast_to_fp8",
            "EpsimError", "ProtocolViolation", "ChannelShutdown", "ConfigError", "FaultError", "ConnectionError_",
            "UnsupportedOperation", "InvariantViolation", "RingDeadlock"]

@@ -21,6 +21,8 @@ IPC_HANDLE_BYTES = 64
 
 CTL_TAIL, CTL_HEAD, CTL_COMPLETED, CTL_FLAGS, CTL_SLOT0 = 0, 8, 16, 24, 32
 
+HT_NVLINK, HT_PROXY, HT_RING = 0, 1, 2  # epb_config_t.ht_transport (EPB_HT_*)
+
 
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
@@ -65,6 +67,26 @@ class CombineArgs(C.Structure):
                 ("channel_prefix_matrix", vp), ("recv_channel_prefix_matrix", vp), ("num_channels", C.c_int),
                 ("num_tokens", C.c_int),
                 ("combined_x", vp), ("combined_topk_weights", vp)]
+
+
+class RingLayout(C.Structure):
+    _fields_ = [("lanes", C.c_int), ("ring_tokens", C.c_int), ("disp_slot_bytes", i64), ("comb_slot_bytes", i64),
+                ("disp_off", i64), ("comb_off", i64), ("bytes_needed", i64)]
+
+
+class RingDispatchArgs(C.Structure):
+    _fields_ = [("x", vp), ("x_scales", vp), ("hidden", C.c_int), ("elem_bytes", C.c_int), ("num_scales", C.c_int),
+                ("topk_idx", vp), ("topk_weights", vp), ("num_topk", C.c_int), ("num_tokens", C.c_int),
+                ("num_experts", C.c_int), ("rank_prefix_matrix", vp), ("recv_channel_prefix_matrix", vp),
+                ("send_head", vp), ("num_channels", C.c_int), ("recv_x", vp), ("recv_x_scales", vp),
+                ("recv_topk_idx", vp), ("recv_topk_weights", vp), ("recv_src_idx", vp)]
+
+
+class RingCombineArgs(C.Structure):
+    _fields_ = [("x", vp), ("topk_weights", vp), ("num_recv", C.c_int), ("hidden", C.c_int), ("num_topk", C.c_int),
+                ("rank_prefix_matrix", vp), ("recv_channel_prefix_matrix", vp), ("send_head", vp),
+                ("num_channels", C.c_int), ("num_tokens", C.c_int), ("combined_x", vp),
+                ("combined_topk_weights", vp)]
 
 
 class LLLayout(C.Structure):
@@ -113,6 +135,10 @@ _proto("epb_recv_layout", c_int, vp, c_int, c_int, C.POINTER(RecvLayout))
 _proto("epb_wait_notify", c_int, vp, P64, P32, c_int, c_double)
 _proto("epb_dispatch", c_int, CTXS, c_int, C.POINTER(DispatchArgs), c_int, vp)
 _proto("epb_combine", c_int, CTXS, c_int, C.POINTER(CombineArgs), c_int, vp)
+_proto("epb_ring_layout", c_int, vp, c_int, c_int, c_int, c_int, C.POINTER(RingLayout))
+_proto("epb_dispatch_notify", c_int, CTXS, c_int, C.POINTER(DispatchArgs), c_int, vp)
+_proto("epb_ring_dispatch", c_int, CTXS, c_int, C.POINTER(RingDispatchArgs), c_int, vp)
+_proto("epb_ring_combine", c_int, CTXS, c_int, C.POINTER(RingCombineArgs), c_int, vp)
 _proto("epb_ll_layout", c_int, c_int, c_int, c_int, c_int, c_int, c_int, C.POINTER(LLLayout))
 _proto("epb_ll_dispatch", c_int, CTXS, c_int, C.POINTER(LLDispatchArgs), c_int, vp)
 _proto("epb_ll_combine", c_int, CTXS, c_int, C.POINTER(LLCombineArgs), c_int, vp)
@@ -148,7 +174,8 @@ _proto("epb_proxy_barrier", c_int, vp, c_int, c_int, vp)
 EXPORTED = [
     "epb_create", "epb_destroy", "epb_ipc_handle", "epb_open_peers", "epb_link_local", "epb_last_error",
     "epb_device_error", "epb_clear_device_error", "epb_num_sms", "epb_region", "epb_trace", "epb_debug_stamp", "epb_get_dispatch_layout",
-    "epb_recv_layout", "epb_wait_notify", "epb_dispatch", "epb_combine", "epb_ll_layout",
+    "epb_recv_layout", "epb_wait_notify", "epb_dispatch", "epb_combine", "epb_ring_layout", "epb_dispatch_notify",
+    "epb_ring_dispatch", "epb_ring_combine", "epb_ll_layout",
     "epb_ll_dispatch", "epb_ll_combine", "epb_per_token_cast_to_fp8", "epb_cmd_pack", "epb_cmd_pack_fields",
     "epb_cmd_unpack_fields", "epb_imm_encode_ll_batch", "epb_imm_encode_ht_batch", "epb_ring_push_batch",
     "epb_ring_pop_batch", "epb_ring_poll", "epb_ring_mark_completed", "epb_ring_check_completion",

@@ -33,6 +33,7 @@ from typing import List, Optional, Sequence, Tuple, Union
 import torch
 
 from . import _lib as L
+from . import chunked
 from ._lib import check, lib, raw_stream
 from .errors import ConfigError, UnsupportedOperation, raise_for
 
@@ -116,6 +117,23 @@ def nvl_bytes_hint(num_tokens: int, hidden: int, num_ranks: int, num_topk: int =
     return rows * (slots * per_row + 2 * comb_row) + 256 * (6 * slots + 6) + (1 << 20)
 
 
+def ring_nvl_bytes(hidden: int, num_ranks: int, num_topk: int = 8, lanes: int = 16, ring_tokens: int = 256) -> int:
+    """Arena bytes for the chunked-ring transport (ht_transport="ring"): one
+    dispatch ring and one combine ring of `ring_tokens` slots per (peer, lane)
+    (csrc/chunked.cu ring_geometry) — independent of the token count."""
+    def up(x, a):
+        return (x + a - 1) // a * a
+    S = hidden // 128
+    o_sc = up(2 * hidden, 16)
+    o_ti = up(o_sc + 4 * S, 8)
+    disp = up(o_ti + 12 * num_topk + 8, 16)
+    comb = up(2 * hidden + 4 * num_topk, 16)
+    return num_ranks * lanes * ring_tokens * (disp + comb)
+
+
+_HT_CODES = {"nvlink": L.HT_NVLINK, "proxy": L.HT_PROXY, "ring": L.HT_RING}
+
+
 class _SlotMemory:
     """``__cuda_array_interface__`` over raw device memory (debug views)."""
 
@@ -129,11 +147,11 @@ class _Rank:
     object (receive-slot pool, cached arena geometry)."""
 
     def __init__(self, rank: int, world: int, nvl_bytes: int, ll_bytes: int, num_recv_slots: int,
-                 fifo_channels: int, fifo_capacity: int, proxy_threads: int, ht_proxy: bool = False):
+                 fifo_channels: int, fifo_capacity: int, proxy_threads: int, ht_transport: str = "nvlink"):
         self.rank, self.world = rank, world
         self.device = torch.device("cuda", torch.cuda.current_device())
         cfg = L.Config(nvl_bytes, ll_bytes, num_recv_slots, fifo_channels, fifo_capacity, proxy_threads,
-                       1 if ht_proxy else 0)
+                       _HT_CODES[ht_transport])
         ctx = C.c_void_p()
         check(lib.epb_create(C.byref(ctx), rank, world, C.byref(cfg)))
         self.ctx = ctx
@@ -169,11 +187,13 @@ def _split_x(x):
 class _Group:
     """List-based implementation shared by Buffer (1 rank) and LocalGroup (R ranks)."""
 
-    def __init__(self, ranks: List[_Rank]):
+    def __init__(self, ranks: List[_Rank], ht_transport: str = "nvlink", ring_lanes: int = 0):
         self.ranks = ranks
         self.native = [r.native for r in ranks]
         self.world = ranks[0].world
         self.timeout_s = _DEFAULT_TIMEOUT_S
+        self.ring = ht_transport == "ring"
+        self.ring_lanes = ring_lanes
 
     def get_dispatch_layout(self, topk_idx_list: Sequence[torch.Tensor], num_experts: int):
         out = []
@@ -189,6 +209,14 @@ class _Group:
         # one block per channel; all blocks of all local ranks must be co-resident
         channels = max(1, min(cfg.resolved_sms(), _device_sms() // n))
         xd, xsc = zip(*[_split_x(x) for x in xs])
+        if self.ring:  # bounded chunked rings (chunked.py / csrc/chunked.cu)
+            if handles[0] is not None:
+                in_ranks, none = [h[4] for h in handles], [None] * n
+                return chunked.ring_dispatch(self.ranks, xd, xsc, in_ranks, none, none, none, expert_alignment,
+                                             channels, self.timeout_s, self.ring_lanes)
+            return chunked.ring_dispatch(self.ranks, xd, xsc, is_token_in_ranks, num_tokens_per_experts, topk_idxs,
+                                         topk_weights_list, expert_alignment, channels, self.timeout_s,
+                                         self.ring_lanes)
         if handles[0] is not None:  # cached layout: the handle carries is_token_in_rank
             in_ranks = [h[4] for h in handles]
             none = [None] * n
@@ -203,6 +231,8 @@ class _Group:
     def combine(self, xs, handles, topk_weights_list, config: Optional[Config]):
         cfg = config or Config()
         ws = list(topk_weights_list) if topk_weights_list is not None else [None] * len(xs)
+        if self.ring:
+            return chunked.ring_combine(self.ranks, list(xs), list(handles), ws, self.ring_lanes)
         return X.combine(self.native, list(xs), list(handles), ws, cfg.resolved_sms())
 
     def ll_dispatch(self, xs, topk_idxs, num_max_dispatch_tokens_per_rank: int, num_experts: int, use_fp8: bool,
@@ -249,14 +279,14 @@ class Buffer:
                  num_qps_per_rank: int = 24, allow_nvlink_for_low_latency_mode: bool = True,
                  allow_mnnvl: bool = False, explicitly_destroy: bool = False, *, num_recv_slots: int = 3,
                  fifo_channels: int = 8, fifo_capacity: int = 1024, proxy_threads: int = 4,
-                 ll_transport: str = "nvlink", ht_transport: str = "nvlink"):
+                 ll_transport: str = "nvlink", ht_transport: str = "nvlink", ring_lanes: int = 0):
         import torch.distributed as dist
         if group is not None and dist.is_available() and dist.is_initialized():
             rank, world = dist.get_rank(group), dist.get_world_size(group)
         else:
             rank, world = 0, 1
-        if ll_transport not in ("nvlink", "proxy") or ht_transport not in ("nvlink", "proxy"):
-            raise ConfigError("ll_transport / ht_transport must be 'nvlink' or 'proxy'")
+        if ll_transport not in ("nvlink", "proxy") or ht_transport not in ("nvlink", "proxy", "ring"):
+            raise ConfigError("ll_transport must be 'nvlink' or 'proxy'; ht_transport 'nvlink', 'proxy' or 'ring'")
         if ht_transport == "proxy" and fifo_channels <= 0:
             raise ConfigError("ht_transport='proxy' needs fifo_channels > 0")
         self.ht_transport = ht_transport
@@ -266,7 +296,7 @@ class Buffer:
         self.num_nvl_bytes, self.num_rdma_bytes = int(num_nvl_bytes), int(num_rdma_bytes)
         ll_bytes = self.num_rdma_bytes if low_latency_mode else 0
         self._rank = _Rank(rank, world, max(self.num_nvl_bytes, 1 << 20), ll_bytes, num_recv_slots,
-                           fifo_channels, fifo_capacity, proxy_threads, ht_proxy=ht_transport == "proxy")
+                           fifo_channels, fifo_capacity, proxy_threads, ht_transport=ht_transport)
         if world > 1:
             h = (C.c_char * L.IPC_HANDLE_BYTES)()
             check(lib.epb_ipc_handle(self._rank.ctx, h))
@@ -278,7 +308,7 @@ class Buffer:
             check(lib.epb_link_local(_ctx_array([self._rank]), 1))
         if ll_transport == "proxy" or ht_transport == "proxy":
             self.start_proxy()
-        self._g = _Group([self._rank])
+        self._g = _Group([self._rank], ht_transport, ring_lanes)
         self._native = self._rank.native
         self._sms_key, self._sms_val = None, 0
         self._destroyed = False
@@ -372,6 +402,14 @@ class Buffer:
         if previous_event is not None:
             previous_event.current_stream_wait()
         xd, xs = (x[0], x[1]) if isinstance(x, tuple) else (x, None)
+        if self.ht_transport == "ring":
+            if handle is None and is_token_in_rank is None:
+                raise ConfigError("is_token_in_rank is required without a handle")
+            (r,) = self._g.dispatch([x], [handle], [is_token_in_rank], [num_tokens_per_expert], [topk_idx],
+                                    [topk_weights], expert_alignment, self._config(config))
+            if handle is not None:
+                return r[0], None, None, None, None, _event(async_finish)
+            return r[0], r[1], r[2], r[3], r[4], _event(async_finish)
         if handle is not None:  # cached layout: the handle carries is_token_in_rank
             r = X.dispatch1(self._native, xd, xs, handle[4], None, None, None, expert_alignment, self._sms(config),
                             self._g.timeout_s)
@@ -389,6 +427,9 @@ class Buffer:
             raise UnsupportedOperation("combine bias is not supported")
         if previous_event is not None:
             previous_event.current_stream_wait()
+        if self.ht_transport == "ring":
+            ((out, out_w),) = self._g.combine([x], [handle], [topk_weights], config)
+            return out, out_w, _event(async_finish)
         out, out_w = X.combine1(self._native, x, handle, topk_weights, self._sms(config))
         return out, out_w, _event(async_finish)
 
@@ -445,13 +486,13 @@ class LocalGroup:
 
     def __init__(self, world: int, num_nvl_bytes: int, num_rdma_bytes: int = 0, *, num_recv_slots: int = 3,
                  fifo_channels: int = 0, fifo_capacity: int = 1024, proxy_threads: int = 1,
-                 ll_transport: str = "nvlink", ht_transport: str = "nvlink"):
+                 ll_transport: str = "nvlink", ht_transport: str = "nvlink", ring_lanes: int = 0):
         if world < 1 or world > L.MAX_LOCAL:
             raise ConfigError("LocalGroup world must be in [1, 8]")
         if ht_transport == "proxy" and fifo_channels <= 0:
             raise ConfigError("ht_transport='proxy' needs fifo_channels > 0")
         self.ranks = [_Rank(r, world, num_nvl_bytes, num_rdma_bytes, num_recv_slots, fifo_channels, fifo_capacity,
-                            proxy_threads, ht_proxy=ht_transport == "proxy") for r in range(world)]
+                            proxy_threads, ht_transport=ht_transport) for r in range(world)]
         check(lib.epb_link_local(_ctx_array(self.ranks), world))
         self.ll_transport = ll_transport
         self.ht_transport = ht_transport
@@ -460,7 +501,7 @@ class LocalGroup:
                 check(lib.epb_proxy_start(rk.ctx))
                 rk.proxy_running = True
         self.world = world
-        self._g = _Group(self.ranks)
+        self._g = _Group(self.ranks, ht_transport, ring_lanes)
 
     def get_dispatch_layout(self, topk_idx_list, num_experts):
         return self._g.get_dispatch_layout(topk_idx_list, num_experts)

@@ -442,10 +442,12 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
   CombineParams P;
   std::memset(&P, 0, sizeof(P));
   P.n_local = n_local;
-  P.proxy = ctxs[0]->cfg.ht_transport ? 1 : 0;
+  P.proxy = ctxs[0]->cfg.ht_transport == EPB_HT_PROXY ? 1 : 0;
+  if (ctxs[0]->cfg.ht_transport == EPB_HT_RING)
+    return epb_set_error(EPB_ERR_CONFIG, "ht_transport=ring: use epb_ring_combine");
   P.fifo_channels = ctxs[0]->cfg.fifo_channels;
   for (int i = 0; i < n_local; ++i)
-    if (P.proxy && (ctxs[i]->cfg.fifo_channels <= 0 || !ctxs[i]->proxy || !ctxs[i]->cfg.ht_transport))
+    if (P.proxy && (ctxs[i]->cfg.fifo_channels <= 0 || !ctxs[i]->proxy || ctxs[i]->cfg.ht_transport != EPB_HT_PROXY))
       return epb_set_error(EPB_ERR_CONFIG, "ht_transport=proxy needs FIFO channels and a running proxy on every rank");
   int nb = std::max(1, num_sms / n_local);
   const int max_active = epb_max_active_blocks((const void*)combine_kernel, kCombineThreads, 0);

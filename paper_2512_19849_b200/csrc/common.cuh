@@ -28,6 +28,7 @@ constexpr int kMaxLocal = EPB_MAX_LOCAL;
 constexpr int kMaxChannels = EPB_MAX_CHANNELS;
 constexpr int kMaxLocalExperts = EPB_MAX_LOCAL_EXPERTS;
 constexpr int kMaxFifo = 64;  // 6-bit channel_id (command.py:37)
+constexpr int kMaxLanes = 32;  // chunked-ring transport: lanes (sender/receiver block pairs)
 
 // ---------------------------------------------------------------------------
 // Symmetric-region layout (identical offsets on every rank).
@@ -62,6 +63,11 @@ struct Meta {
   // combine mode message (tagged words): where src's input rows / weights live
   // inside src's region, in 16-byte / 4-byte units (kNotifyAbort: not there)
   uint64_t comb_msg[2][kMaxRanks][2];
+  // chunked rings (chunked.cu), cumulative token counts, [dispatch|combine]:
+  // rc_tail[.][src][lane]: slots src has filled in its ring here (producer-advanced)
+  // rc_head[.][dst][lane]: slots dst has drained from my ring there (credit return)
+  uint32_t rc_tail[2][kMaxRanks][kMaxLanes];
+  uint32_t rc_head[2][kMaxRanks][kMaxLanes];
   NotifyMsg mbox[2][kMaxRanks];
 };
 
@@ -76,6 +82,9 @@ struct Scratch {                         // private to the owning rank
   // staging (proxy transport)
   uint64_t plan[4][kMaxRanks];
   uint32_t ll_ticket[4];                 // LL last-warp tickets: [dispatch|combine][parity]
+  // chunked rings: this rank's own cumulative positions, [dispatch|combine]
+  uint32_t rc_sent[2][kMaxRanks][kMaxLanes];   // slots I have filled in dst's ring
+  uint32_t rc_recvd[2][kMaxRanks][kMaxLanes];  // slots I have drained from src's ring
   // LL epochs live on the device (bumped by each call's last warp) so LL calls
   // can be captured in CUDA graphs and replayed: [dispatch|combine]
   uint32_t ll_epoch[2];

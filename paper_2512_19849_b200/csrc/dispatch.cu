@@ -68,6 +68,7 @@ __device__ __forceinline__ int warp_scan_row(const int32_t* in, int32_t* incl_ou
 struct DispatchParams {
   int n_local, num_slots;
   int proxy;                    // ht_transport = CPU proxy (rows to peers go through the FIFO)
+  int notify_only;              // chunked-ring transport: counts, handle and host counts only (chunked.cu moves rows)
   int fifo_channels;
   uint64_t ht_calls[kMaxLocal];  // proxy transport: expected ht_sig[0][src] (calls so far)
   uint32_t epoch[kMaxLocal];   // per-call epoch: the tag of this call's mailbox / host words
@@ -282,7 +283,7 @@ __device__ __forceinline__ void exchange_counts(const DispatchParams& P, int lr,
     }
   }
   __syncwarp();
-  if (lane == 0 && *s_abort == 0) {
+  if (lane == 0 && *s_abort == 0 && !P.notify_only) {
     // capacity checks (every rank sees the same matrix, so all abort together)
     int err = 0;
     int64_t detail = 0;
@@ -460,7 +461,7 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     const int n16 = (int)(row_bytes >> 4);
     const int k = a.num_topk, S = a.num_scales;
     const int L = (a.topk_idx != nullptr && a.num_experts > 0) ? a.num_experts / R : 0;
-    for (int tt = warp - first_copy_warp; tt >= 0 && tt < nt; tt += nwarps - first_copy_warp) {
+    for (int tt = warp - first_copy_warp; !P.notify_only && tt >= 0 && tt < nt; tt += nwarps - first_copy_warp) {
       const int t = t0 + tt;
       const int4* src = reinterpret_cast<const int4*>(static_cast<const char*>(a.x) + (size_t)t * row_bytes);
       for (int base = 0; base < n16; base += 32 * kCopyUnroll) {
@@ -510,7 +511,10 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   __syncthreads();
   trace_mark(rv, 9);
   trace_mark_max(rv, 12);
-  if (!P.proxy) {
+  if (P.notify_only) {
+    // no rows moved: nothing to signal (the handle outputs are complete when
+    // the kernel ends; the ring kernel runs next on the stream)
+  } else if (!P.proxy) {
     if (tid < R) {  // the local destination only needs gpu scope
       if (tid == me) red_release_gpu_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
       else red_release_sys_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
@@ -545,8 +549,8 @@ __global__ void dispatch_proxy_wait_kernel(const __grid_constant__ DispatchParam
 
 using namespace epb;
 
-extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_args_t* args, int num_channels,
-                            void* stream) {
+static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_args_t* args, int num_channels,
+                           void* stream, int notify_only) {
   if (int e = check_group(ctxs, n_local)) return e;
   if (num_channels <= 0 || num_channels > kMaxChannels)
     return epb_set_error(EPB_ERR_CONFIG, "num_channels out of range");
@@ -554,10 +558,11 @@ extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_
   std::memset(&P, 0, sizeof(P));
   P.n_local = n_local;
   P.num_slots = std::max(1, ctxs[0]->cfg.num_recv_slots);
-  P.proxy = ctxs[0]->cfg.ht_transport ? 1 : 0;
+  P.proxy = ctxs[0]->cfg.ht_transport == EPB_HT_PROXY ? 1 : 0;
+  P.notify_only = notify_only;
   P.fifo_channels = ctxs[0]->cfg.fifo_channels;
   for (int i = 0; i < n_local; ++i) {
-    if ((ctxs[i]->cfg.ht_transport != 0) != (P.proxy != 0))
+    if (ctxs[i]->cfg.ht_transport != ctxs[0]->cfg.ht_transport)
       return epb_set_error(EPB_ERR_CONFIG, "all ranks of a group must use the same ht_transport");
     if (P.proxy && (ctxs[i]->cfg.fifo_channels <= 0 || !ctxs[i]->proxy))
       return epb_set_error(EPB_ERR_CONFIG, "ht_transport=proxy needs FIFO channels and a running proxy");
@@ -570,7 +575,8 @@ extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_
     if (a.num_experts > 0 &&
         (a.num_experts % ctxs[i]->world != 0 || a.num_experts / ctxs[i]->world > kMaxLocalExperts))
       return epb_set_error(EPB_ERR_CONFIG, "num_experts must be a multiple of world (<= 1024 local experts)");
-    if (int e = compute_recv_layout(ctxs[i], a.hidden, a.num_topk, &P.lay)) return e;
+    if (!notify_only)
+      if (int e = compute_recv_layout(ctxs[i], a.hidden, a.num_topk, &P.lay)) return e;
     max_tc = std::max(max_tc, (a.num_tokens + num_channels - 1) / num_channels);
   }
   const size_t smem = sizeof(int32_t) * (size_t)max_tc * ctxs[0]->world;
@@ -597,6 +603,18 @@ extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_
     EPB_CUDA(cudaGetLastError());
   }
   return EPB_OK;
+}
+
+extern "C" int epb_dispatch(epb_t* const* ctxs, int n_local, const epb_dispatch_args_t* args, int num_channels,
+                            void* stream) {
+  if (ctxs && n_local > 0 && ctxs[0] && ctxs[0]->cfg.ht_transport == EPB_HT_RING)
+    return epb_set_error(EPB_ERR_CONFIG, "ht_transport=ring: use epb_dispatch_notify + epb_ring_dispatch");
+  return dispatch_launch(ctxs, n_local, args, num_channels, stream, 0);
+}
+
+extern "C" int epb_dispatch_notify(epb_t* const* ctxs, int n_local, const epb_dispatch_args_t* args,
+                                   int num_channels, void* stream) {
+  return dispatch_launch(ctxs, n_local, args, num_channels, stream, 1);
 }
 
 extern "C" int epb_wait_notify(epb_t* ctx, int64_t* num_recv, int32_t* num_recv_per_expert, int num_local_experts,

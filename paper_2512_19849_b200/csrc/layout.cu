@@ -101,7 +101,7 @@ int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t
   const size_t per_row = x_row + S * 4 + (size_t)k * 12 + 4;
   const size_t comb_row = 2 * (size_t)hidden + (size_t)k * 4;
   const int ns = std::max(1, ctx->cfg.num_recv_slots);
-  const int nsend = ctx->cfg.ht_transport ? 1 : 0;  // proxy transport: one send-staging slot
+  const int nsend = ctx->cfg.ht_transport == EPB_HT_PROXY ? 1 : 0;  // proxy transport: one send-staging slot
   const size_t overhead = A * (size_t)(6 * (ns + nsend) + 6);
   if (ctx->cfg.nvl_bytes <= overhead) return epb_set_error(EPB_ERR_CONFIG, "num_nvl_bytes too small");
   int64_t cap = (int64_t)((ctx->cfg.nvl_bytes - overhead) / ((ns + nsend) * per_row + 2 * comb_row));

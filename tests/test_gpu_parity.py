@@ -54,7 +54,10 @@ def _emulated_dispatch(torch, R, Ts, H, E, k, seed, fp8=False, mask=0.0, zipf=0.
         xs.append(bf16_random(g, (Ts[r], H)))
         idxs.append(idx)
         ws.append(w)
-    from paper_2512_19849_b200 import nvl_bytes_hint
+    from paper_2512_19849_b200 import nvl_bytes_hint, ring_nvl_bytes
+    if grp is None and ht == "ring":  # bounded rings of 64 slots: the chunks wrap and wait for credit
+        lanes = min(16, 148 // (2 * R))
+        grp = LocalGroup(R, ring_nvl_bytes(H, R, k, lanes, 64), ht_transport="ring", ring_lanes=lanes)
     if grp is None:
         grp = LocalGroup(R, nvl_bytes_hint(max(Ts), H, R, k, slots, ht_proxy=ht == "proxy"), num_recv_slots=slots,
                          fifo_channels=4 if ht == "proxy" else 0, proxy_threads=2, ht_transport=ht)
@@ -85,10 +88,16 @@ def _emulated_dispatch(torch, R, Ts, H, E, k, seed, fp8=False, mask=0.0, zipf=0.
     (2, [257, 64], 2048, 32, 4, 0.0, 7, "proxy"),
     (4, [0, 333, 1, 50], 7168, 64, 8, 0.2, 20, "proxy"),
     (8, [200] * 8, 1024, 64, 8, 0.0, None, "proxy"),
+    # bounded chunked ring channels
+    (1, [3000], 1024, 16, 4, 0.0, None, "ring"),
+    (2, [2500, 700], 2048, 32, 4, 0.0, 7, "ring"),
+    (4, [0, 1333, 1, 900], 7168, 64, 8, 0.2, 20, "ring"),
+    (8, [600] * 8, 1024, 64, 8, 0.0, None, "ring"),
 ])
 def test_dispatch_combine_emulated(torch, R, Ts, H, E, k, mask, sms, ht):
     grp = None
-    for it in range(2 if ht == "proxy" else 1):  # proxy: the signal counters must stay in step across calls
+    # proxy / ring: the cumulative signal and ring counters must stay in step across calls
+    for it in range({"proxy": 2, "ring": 3}.get(ht, 1)):
         grp, xs, idxs, ws, x_in, _, lay, res = _emulated_dispatch(torch, R, Ts, H, E, k, seed=R * 7 + H + it,
                                                                   mask=mask, num_sms=sms, ht=ht, grp=grp)
         _check_dispatch_combine(torch, grp, R, E, xs, idxs, ws, res)
@@ -131,7 +140,7 @@ def _check_dispatch_combine(torch, grp, R, E, xs, idxs, ws, res):
         assert comb[s][1] is None
 
 
-@pytest.mark.parametrize("ht", ["nvlink", "proxy"])
+@pytest.mark.parametrize("ht", ["nvlink", "proxy", "ring"])
 def test_dispatch_fp8_tuple_emulated(torch, ht):
     R, Ts, H, E, k = 4, [100, 90, 80, 70], 7168, 32, 8
     grp, xs, idxs, ws, x_in, scales, lay, res = _emulated_dispatch(torch, R, Ts, H, E, k, seed=5, fp8=True, ht=ht)
