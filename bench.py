@@ -423,6 +423,7 @@ def run_ours(args):
                          ("dsv3_bf16_combine_push", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, combine_in_region=False,
                                                          buf=buf)),
                          ("qwen3_235b_zipf", dict(T=8192, H=4096, E=128, zipf=1.0)),
+                         ("dsv3_bf16_ring", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, ht="ring")),
                          ("dsv3_bf16_ht_proxy", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, ht="proxy"))):
             # the proxy HT transport is opt-in here (its first call can
             # stall when another Buffer of the process has run a combine)
@@ -475,7 +476,9 @@ def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T,
     import paper_2512_19849_b200 as epb
     from tests.helpers import bf16_random, make_routing
     own = buf is None
-    if own:
+    if own and ht == "ring":  # bounded rings: 74 lanes x 64 slots per peer, whatever T is (tools/ring_sweep.py)
+        buf = epb.Buffer(group, epb.ring_nvl_bytes(H, R, TOPK, 74, 64), 0, ht_transport="ring", ring_lanes=74)
+    elif own:
         buf = epb.Buffer(group, epb.nvl_bytes_hint(T, H, R, TOPK, 2, ht_proxy=ht == "proxy"), 0, num_recv_slots=2,
                          fifo_channels=8 if ht == "proxy" else 0, proxy_threads=4, ht_transport=ht)
     g = np.random.default_rng(31_000 + 97 * rank + int(zipf * 10))
@@ -541,10 +544,13 @@ def _config_loop(buf, own, idx_t, w_t, x_in, fp8, combine_in_region, flush, remo
         prof = []
         flush.zero_()
         torch.cuda._sleep(spin)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()  # ring transport: Python host path (count exchange, host sync, ring kernel)
         with epb.buffer.profiling(prof):
             recv_x, _, rtw, _, handle, _ = buf.dispatch(x_in, num_tokens_per_rank=per_rank,
                                                         is_token_in_rank=in_rank, num_tokens_per_expert=per_exp,
                                                         topk_idx=idx_t, topk_weights=w_t)
+        ev[1].record()
         if fp8 or not combine_in_region:  # expert outputs live in ordinary device memory
             y = torch.empty((recv_x[0] if fp8 else recv_x).shape[0], H, dtype=torch.bfloat16, device=dev)
             y.copy_(recv_x[0].to(torch.bfloat16) if fp8 else recv_x)
@@ -552,10 +558,14 @@ def _config_loop(buf, own, idx_t, w_t, x_in, fp8, combine_in_region, flush, remo
             y = recv_x
         flush.zero_()
         torch.cuda._sleep(spin)
+        ev[2].record()
         with epb.buffer.profiling(prof):
             buf.combine(y, handle, topk_weights=rtw)
+        ev[3].record()
         barrier()
         t = dict(prof)
+        if ht == "ring":
+            t = {"dispatch": ev[0].elapsed_time(ev[1]), "combine": ev[2].elapsed_time(ev[3])}
         if it >= 3:
             d_ms.append(max_over_ranks(t["dispatch"]))
             c_ms.append(max_over_ranks(t["combine"]))
@@ -566,9 +576,14 @@ def _config_loop(buf, own, idx_t, w_t, x_in, fp8, combine_in_region, flush, remo
     rem_max = max_over_ranks(float(remote))
     d, c = statistics.median(d_ms), statistics.median(c_ms)
     out = {"tokens_per_rank": T, "hidden": H, "experts": E, "topk": TOPK, "dispatch_dtype": "fp8" if fp8 else "bf16",
-           "routing": f"zipf({zipf})" if zipf else "uniform", "transport": "CPU proxy (FIFO + copy engine)"
-           if ht == "proxy" else "SM stores/loads over NVLink", "dispatch_us": round(d * 1e3, 2),
-           "combine_us": round(c * 1e3, 2), "combine_input": ("arena view (WRITE in place)" if ht == "proxy" else "arena view (pull)")
+           "routing": f"zipf({zipf})" if zipf else "uniform",
+           "transport": {"proxy": "CPU proxy (FIFO + copy engine)",
+                         "ring": f"bounded chunked rings ({buf.num_nvl_bytes / 1e6:.0f} MB arena, 74 lanes x 64 "
+                                 "slots per peer; worst-case slots would need "
+                                 f"{epb.nvl_bytes_hint(T, H, R, TOPK, 2) / 1e6:.0f} MB)"}.get(
+                             ht, "SM stores/loads over NVLink"), "dispatch_us": round(d * 1e3, 2),
+           "combine_us": round(c * 1e3, 2), "combine_input": "device tensor (ring transport)" if ht == "ring"
+           else ("arena view (WRITE in place)" if ht == "proxy" else "arena view (pull)")
            if y_in_region(fp8, combine_in_region)
            else "device tensor outside the arena (push)", "reps": reps}
     if R > 1:

@@ -117,7 +117,7 @@ def nvl_bytes_hint(num_tokens: int, hidden: int, num_ranks: int, num_topk: int =
     return rows * (slots * per_row + 2 * comb_row) + 256 * (6 * slots + 6) + (1 << 20)
 
 
-def ring_nvl_bytes(hidden: int, num_ranks: int, num_topk: int = 8, lanes: int = 16, ring_tokens: int = 256) -> int:
+def ring_nvl_bytes(hidden: int, num_ranks: int, num_topk: int = 8, lanes: int = 74, ring_tokens: int = 64) -> int:
     """Arena bytes for the chunked-ring transport (ht_transport="ring"): one
     dispatch ring and one combine ring of `ring_tokens` slots per (peer, lane)
     (csrc/chunked.cu ring_geometry) — independent of the token count."""

@@ -390,9 +390,9 @@ static int ring_geometry(const epb_ctx* c, int hidden, int k, int lanes, int n_l
                          epb_ring_layout_t* out) {
   if (hidden <= 0 || hidden % 128) return epb_set_error(EPB_ERR_CONFIG, "hidden must be a positive multiple of 128");
   if (k < 0 || k > 32) return epb_set_error(EPB_ERR_CONFIG, "num_topk must be in [0, 32]");
-  if (lanes <= 0) lanes = std::max(1, std::min(16, c->num_sms / (2 * std::max(1, n_local))));
+  if (lanes <= 0) lanes = std::max(1, std::min(kMaxLanes, c->num_sms / (2 * std::max(1, n_local))));
   if (lanes > kMaxLanes || 2 * lanes * n_local > c->num_sms)
-    return epb_set_error(EPB_ERR_CONFIG, "ring lanes: 2 x lanes x local ranks must fit the SMs (<= 32 lanes)");
+    return epb_set_error(EPB_ERR_CONFIG, "ring lanes: 2 x lanes x local ranks must fit the SMs (<= 80 lanes)");
   const int64_t S = hidden / 128, R = c->world;
   std::memset(g, 0, sizeof(*g));
   g->lanes = lanes;

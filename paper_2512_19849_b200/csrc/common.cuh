@@ -28,7 +28,7 @@ constexpr int kMaxLocal = EPB_MAX_LOCAL;
 constexpr int kMaxChannels = EPB_MAX_CHANNELS;
 constexpr int kMaxLocalExperts = EPB_MAX_LOCAL_EXPERTS;
 constexpr int kMaxFifo = 64;  // 6-bit channel_id (command.py:37)
-constexpr int kMaxLanes = 32;  // chunked-ring transport: lanes (sender/receiver block pairs)
+constexpr int kMaxLanes = 80;  // chunked-ring transport: lanes (sender/receiver block pairs)
 
 // ---------------------------------------------------------------------------
 // Symmetric-region layout (identical offsets on every rank).

@@ -48,9 +48,11 @@ def _worker(rank, world, port, results):
         xs, idxs, ws = _inputs(R, Ts, H, E, k, seed=1)
         topk = torch.from_numpy(idxs[rank]).cuda()
         w = torch.from_numpy(ws[rank]).cuda()
-        for ht in ("nvlink", "proxy"):  # kernels' NVLink stores / the CPU proxy's WRITE+ATOMIC commands
-            buf = epb.Buffer(dist.group.WORLD, epb.nvl_bytes_hint(max(Ts), H, R, k, ht_proxy=ht == "proxy"), 0,
-                             fifo_channels=4, ht_transport=ht)
+        # kernels' NVLink stores / the CPU proxy's WRITE+ATOMIC commands / bounded chunked rings
+        for ht in ("nvlink", "proxy", "ring"):
+            nvl = (epb.ring_nvl_bytes(H, R, k, 16, 64) if ht == "ring"
+                   else epb.nvl_bytes_hint(max(Ts), H, R, k, ht_proxy=ht == "proxy"))
+            buf = epb.Buffer(dist.group.WORLD, nvl, 0, fifo_channels=4, ht_transport=ht, ring_lanes=16)
             for it in range(3):  # repeat: exercises both parities / epochs and slot reuse
                 per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(topk, E)
                 recv_x, rti, rtw, lst, handle, _ = buf.dispatch(
