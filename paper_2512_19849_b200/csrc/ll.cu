@@ -130,12 +130,15 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     uint32_t* bm = reinterpret_cast<uint32_t*>(smem);
     int32_t* cnt = reinterpret_cast<int32_t*>(bm + (size_t)E * W);
     int32_t* pre = cnt + E;
+    int16_t* s_e = reinterpret_cast<int16_t*>(pre + E);  // [T][k] expert ids (-1: masked), read by the items
     for (int i = tid; i < E * W; i += blockDim.x) bm[i] = 0;
     __syncthreads();
     for (int i = tid; i < T * k; i += blockDim.x) {
       const int64_t e = a.topk_idx[i];
       const int t = i / k;
-      if (e >= 0 && e < E) atomicOr(&bm[(size_t)e * W + (t >> 5)], 1u << (t & 31));
+      const bool ok = e >= 0 && e < E;
+      s_e[i] = ok ? (int16_t)e : (int16_t)-1;
+      if (ok) atomicOr(&bm[(size_t)e * W + (t >> 5)], 1u << (t & 31));
     }
     __syncthreads();
     for (int e = tid; e < E; e += blockDim.x) {
@@ -152,20 +155,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     const int NCH = (H + kChunkCh - 1) / kChunkCh;
     for (int item = blockIdx.x * nw + warp; item < T * NCH; item += total_w) {
       const int t = item / NCH, ch = item % NCH;
-      uint64_t p = 0;
-      if (lane < k) {
-        const int64_t e = a.topk_idx[(size_t)t * k + lane];
-        int32_t slot = -1;
-        if (e >= 0 && e < E) {
-          const int d = (int)(e / L);
-          const int row = pre[e] + ordinal_of(bm + (size_t)e * W, t);
-          char* blk = P.use_proxy ? my_ll + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block
-                                  : rv.peer[d] + P.ll_off + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
-          p = reinterpret_cast<uint64_t>(blk + g.hdr_bytes + (int64_t)row * rstride);
-          slot = (int32_t)(d * g.rows_per_src + row);
-        }
-        if (ch == 0) a.comb_slot[(size_t)t * k + lane] = slot;
-      }
+      // the token's HBM loads first, so their latency overlaps the slot math
       const int ch0 = ch * kChunkCh + lane * 16;
       const bool active = ch0 < H;
       const int4* src = reinterpret_cast<const int4*>(static_cast<const char*>(a.x) + (size_t)t * H * 2);
@@ -173,6 +163,20 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       if (active) {
         x0 = ld_nc_v4(src + ch0 / 8);
         x1 = ld_nc_v4(src + ch0 / 8 + 1);
+      }
+      uint64_t p = 0;
+      if (lane < k) {
+        const int e = s_e[t * k + lane];
+        int32_t slot = -1;
+        if (e >= 0) {
+          const int d = e / L;
+          const int row = pre[e] + ordinal_of(bm + (size_t)e * W, t);
+          char* blk = P.use_proxy ? my_ll + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block
+                                  : rv.peer[d] + P.ll_off + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
+          p = reinterpret_cast<uint64_t>(blk + g.hdr_bytes + (int64_t)row * rstride);
+          slot = (int32_t)(d * g.rows_per_src + row);
+        }
+        if (ch == 0) a.comb_slot[(size_t)t * k + lane] = slot;
       }
       if (g.use_fp8) {
         int4 q;
@@ -405,25 +409,39 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
   }
 
   if (P.phases & 2) {
+    const int T = a.num_tokens;
+    const int NCC = (n16 + 63) / 64;  // 64 x 16 B columns per item (2 per lane)
+    // each warp's first two items: their routing slots and weights are loaded
+    // before the wait for the peers, off the critical path
+    int pre_slot[2] = {-1, -1};
+    float pre_w[2] = {0.0f, 0.0f};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int item = blockIdx.x * nw + warp + q * total_w;
+      if (item < T * NCC && lane < k) {
+        const int t = item / NCC;
+        pre_slot[q] = a.comb_slot[(size_t)t * k + lane];
+        pre_w[q] = a.topk_weights[(size_t)t * k + lane];
+      }
+    }
     if (tid < R) {
       if (!P.use_proxy) wait_geq(rv, &my_meta->ll_comb_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x700 + tid);
       else wait_geq64(rv, &my_meta->proxy_sig[P.disp_channels + me % P.disp_channels][tid], pexp, 0x780 + tid);
     }
     __syncthreads();
     trace_mark(rv, 34);
-    const int T = a.num_tokens;
-    const int NCC = (n16 + 63) / 64;  // 64 x 16 B columns per item (2 per lane)
     const char* recv = my_ll + g.off_comb_recv + (int64_t)par * R * g.comb_block;
-    for (int item = blockIdx.x * nw + warp; item < T * NCC; item += total_w) {
+    int q = 0;
+    for (int item = blockIdx.x * nw + warp; item < T * NCC; item += total_w, ++q) {
       const int t = item / NCC, i0 = (item % NCC) * 64 + lane, i1 = i0 + 32;
       uint64_t p = 0;
       float w = 0.0f;
       if (lane < k) {
-        const int slot = a.comb_slot[(size_t)t * k + lane];
+        const int slot = q < 2 ? pre_slot[q] : a.comb_slot[(size_t)t * k + lane];
         if (slot >= 0) {
           const int r = (int)(slot / g.rows_per_src), row = (int)(slot % g.rows_per_src);
           p = reinterpret_cast<uint64_t>(recv + (int64_t)r * g.comb_block + (int64_t)row * g.comb_row);
-          w = a.topk_weights[(size_t)t * k + lane];
+          w = q < 2 ? pre_w[q] : a.topk_weights[(size_t)t * k + lane];
         }
       }
       float acc0[8], acc1[8];
@@ -571,7 +589,7 @@ extern "C" int epb_ll_dispatch(epb_t* const* ctxs, int n_local, const epb_ll_dis
     P.a[i] = args[i];
   }
   const int W = std::max(1, (a0.max_tokens + 31) / 32);
-  const size_t smem_send = ((size_t)P.g.E * W + 2 * P.g.E) * 4;
+  const size_t smem_send = ((size_t)P.g.E * W + 2 * P.g.E) * 4 + (size_t)a0.max_tokens * a0.num_topk * 2;
   const size_t smem_recv = (size_t)(3 * P.g.R * P.g.L + P.g.L + 1) * 4;
   const size_t smem = std::max(smem_send, smem_recv);
   if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "LL dispatch shape needs too much shared memory");
