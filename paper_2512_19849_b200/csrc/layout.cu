@@ -5,11 +5,17 @@
 // token goes once to every distinct destination rank among its top-k
 // experts (on one NVLink node "node" == rank).
 //
-// One cooperative kernel (no separate memset launch): block 0 zeroes the
-// count outputs while every block stages its [tokens x k] tile with 16-byte
-// loads and histograms it in shared memory (rank counts are warp-aggregated
-// with __ballot_sync + popc); a grid barrier then orders the zeroing before
-// the blocks' global atomics.
+// Primary kernel: ONE thread-block cluster of 16 blocks (B200's largest,
+// opt-in non-portable size).  Every block stages its slice of the [tokens x k]
+// top-k matrix with 16-byte loads, writes is_token_in_rank and builds its
+// (expert, rank) histogram in shared memory; after a cluster barrier each
+// block sums one slice of the histogram across all 16 blocks through
+// distributed shared memory and stores the counts: no zeroing pass, no global
+// atomics, no grid barrier.
+//
+// Fallback (if the cluster launch is refused): one cooperative kernel; block
+// 0 zeroes the count outputs while every block histograms its tile, a grid
+// barrier orders the zeroing before the blocks' global atomics.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -85,6 +91,87 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(const int64_t* _
     if (s_hist[E + i]) atomicAdd(&per_rank[i], s_hist[E + i]);
 }
 
+constexpr int kClusterBlocks = 16;
+constexpr int kClusterThreads = 256;
+
+__global__ void __launch_bounds__(kClusterThreads, 1)
+    layout_cluster_kernel(const int64_t* __restrict__ topk_idx, int T, int k, int E, int R,
+                          int32_t* __restrict__ per_rank, int32_t* __restrict__ per_expert,
+                          uint8_t* __restrict__ in_rank) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ int64_t s_dyn[];
+  int64_t* s_topk = s_dyn;                                                        // [blockDim * k]
+  int32_t* s_hist = reinterpret_cast<int32_t*>(s_topk + (size_t)blockDim.x * k);  // [E + R]
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nb = (int)cluster.num_blocks(), b = (int)cluster.block_rank();
+  for (int i = tid; i < E + R; i += blockDim.x) s_hist[i] = 0;
+  const int L = E / R;
+  for (int t_first = b * blockDim.x; t_first < T; t_first += nb * blockDim.x) {
+    const int n_tok = min((int)blockDim.x, T - t_first);
+    const int n_words = n_tok * k;
+    const int64_t* src = topk_idx + (size_t)t_first * k;
+    __syncthreads();
+    if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (n_words % 2 == 0)) {
+      // every 16-byte load of the tile in flight at once (k <= 32: <= 16 per thread)
+      constexpr int kPer = 16;
+      int4 v[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = tid + u * (int)blockDim.x;
+        if (i < n_words / 2) v[u] = __ldg(reinterpret_cast<const int4*>(src) + i);
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = tid + u * (int)blockDim.x;
+        if (i < n_words / 2) reinterpret_cast<int4*>(s_topk)[i] = v[u];
+      }
+    } else {
+      for (int i = tid; i < n_words; i += blockDim.x) s_topk[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const int t = t_first + tid;
+    const bool valid = t < T;
+    uint32_t mask = 0;
+    for (int j = 0; j < k; ++j) {
+      const int64_t e64 = valid ? s_topk[tid * k + j] : -1;
+      const int e = (e64 >= 0 && e64 < E) ? (int)e64 : -1;  // out-of-range experts are treated as masked
+      if (e >= 0) {
+        mask |= 1u << (e / L);
+        atomicAdd(&s_hist[e], 1);
+      }
+    }
+    if (valid) {
+      if (R == 8) {
+        uint64_t packed = 0;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) packed |= (uint64_t)((mask >> d) & 1u) << (8 * d);
+        *reinterpret_cast<uint64_t*>(in_rank + (size_t)t * 8) = packed;
+      } else {
+        for (int d = 0; d < R; ++d) in_rank[(size_t)t * R + d] = (mask >> d) & 1u;
+      }
+    }
+    for (int d = 0; d < R; ++d) {
+      const unsigned bal = __ballot_sync(0xffffffffu, (mask >> d) & 1u);
+      if (lane == 0 && bal) atomicAdd(&s_hist[E + d], __popc(bal));
+    }
+  }
+  cluster.sync();  // every block's histogram is complete and visible cluster-wide
+  // block b sums entries [lo, hi) of the (E + R) histogram over the cluster
+  const int n = E + R, lo = (int)((int64_t)n * b / nb), hi = (int)((int64_t)n * (b + 1) / nb);
+  for (int i = lo + tid; i < hi; i += blockDim.x) {
+    int part[kClusterBlocks];
+#pragma unroll
+    for (int q = 0; q < kClusterBlocks; ++q) part[q] = q < nb ? cluster.map_shared_rank(s_hist, q)[i] : 0;
+    int sum = 0;
+#pragma unroll
+    for (int q = 0; q < kClusterBlocks; ++q) sum += part[q];
+    if (i < E) per_expert[i] = sum;
+    else per_rank[i - E] = sum;
+  }
+  cluster.sync();  // no block leaves while a peer may still read its shared memory
+}
+
 }  // namespace epb
 
 using namespace epb;
@@ -153,6 +240,42 @@ extern "C" int epb_get_dispatch_layout(const int64_t* topk_idx, int num_tokens, 
     return epb_set_error(EPB_ERR_CONFIG, "num_experts must be a positive multiple of num_ranks");
   if (num_topk <= 0 || num_topk > 32) return epb_set_error(EPB_ERR_CONFIG, "num_topk must be in [1, 32]");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  {
+    // one 16-block cluster (B200 opt-in size); refused once -> cooperative fallback
+    static int cluster_ok = -1;
+    const size_t csmem = sizeof(int64_t) * kClusterThreads * num_topk + sizeof(int32_t) * (num_experts + num_ranks);
+    if (cluster_ok != 0 && csmem <= 200 * 1024) {
+      cudaError_t e = cudaSuccess;
+      if (cluster_ok < 0) {
+        e = cudaFuncSetAttribute((const void*)layout_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute((const void*)layout_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024);
+      }
+      if (e == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kClusterBlocks);
+        cfg.blockDim = dim3(kClusterThreads);
+        cfg.dynamicSmemBytes = csmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kClusterBlocks;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, layout_cluster_kernel, topk_idx, num_tokens, num_topk, num_experts, num_ranks,
+                               num_tokens_per_rank, num_tokens_per_expert, is_token_in_rank);
+      }
+      if (e == cudaSuccess) {
+        cluster_ok = 1;
+        return EPB_OK;
+      }
+      cudaGetLastError();
+      cluster_ok = 0;
+    }
+  }
   static const int threads = [] {
     const char* s = std::getenv("EPB_LAYOUT_THREADS");
     const int v = s ? std::atoi(s) : 128;
