@@ -117,14 +117,27 @@ __device__ __forceinline__ void reduce_rows(const RowSrc& rs, uint32_t mask, con
   }
 }
 
+// Fan-in >= 2 runs out of line: its own register allocation keeps the
+// kernel body (and the inlined fan-in 1 copy of the EP=1 path) free of spills.
+template <int NV>
+__device__ __noinline__ void reduce_rows_call(const RowSrc& rs, uint32_t mask, const int32_t* sh, int4* out, int n16,
+                                              int lane) {
+  reduce_rows<NV>(rs, mask, sh, out, n16, lane);
+}
+
 __device__ __forceinline__ void zero_row(int4* out, int n16, int lane) {
   for (int i = lane; i < n16; i += 32) st_na_v4(out + i, make_int4(0, 0, 0, 0));
 }
 
 // Phase B: reduce my tokens.  pull: partial d is read in place from d's input
 // (over NVLink); else from my staging, where the sources pushed their rows.
+// send_head rows of a block's tokens, loaded at kernel entry (their latency
+// overlaps the mode exchange / barrier); blocks with more tokens read global
+constexpr int kShTokens = 64;
+
 __device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bool pull, const int64_t* s_xoff,
-                                              const int64_t* s_woff, const int32_t* s_excl, const int32_t* s_mypre) {
+                                              const int64_t* s_woff, const int32_t* s_excl, const int32_t* s_mypre,
+                                              const int32_t (*s_sh)[kMaxRanks]) {
   const RankView& rv = P.rv[lr];
   const epb_combine_args_t& a = P.a[lr];
   const int R = rv.world, me = rv.rank, nb = gridDim.x, b = blockIdx.x;
@@ -156,8 +169,9 @@ __device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bo
     }
   }
   __syncthreads();
+  const bool cached = tb1 - tb0 <= kShTokens;
   for (int t = tb0 + warp; t < tb1; t += nwarps) {
-    const int32_t* sh = a.send_head + (size_t)t * R;
+    const int32_t* sh = cached ? s_sh[t - tb0] : a.send_head + (size_t)t * R;
     // contributing ranks as a bitmask; rows are taken in ascending rank order
     // (the canonical sum order) via __fns inside reduce_rows
     uint32_t mask = 0;
@@ -166,13 +180,13 @@ __device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bo
     int4* out = reinterpret_cast<int4*>(static_cast<char*>(a.combined_x) + (size_t)t * row_bytes);
     switch (__popc(mask)) {
       case 1: reduce_rows<1>(rs, mask, sh, out, n16, lane); break;
-      case 2: reduce_rows<2>(rs, mask, sh, out, n16, lane); break;
-      case 3: reduce_rows<3>(rs, mask, sh, out, n16, lane); break;
-      case 4: reduce_rows<4>(rs, mask, sh, out, n16, lane); break;
-      case 5: reduce_rows<5>(rs, mask, sh, out, n16, lane); break;
-      case 6: reduce_rows<6>(rs, mask, sh, out, n16, lane); break;
-      case 7: reduce_rows<7>(rs, mask, sh, out, n16, lane); break;
-      case 8: reduce_rows<8>(rs, mask, sh, out, n16, lane); break;
+      case 2: reduce_rows_call<2>(rs, mask, sh, out, n16, lane); break;
+      case 3: reduce_rows_call<3>(rs, mask, sh, out, n16, lane); break;
+      case 4: reduce_rows_call<4>(rs, mask, sh, out, n16, lane); break;
+      case 5: reduce_rows_call<5>(rs, mask, sh, out, n16, lane); break;
+      case 6: reduce_rows_call<6>(rs, mask, sh, out, n16, lane); break;
+      case 7: reduce_rows_call<7>(rs, mask, sh, out, n16, lane); break;
+      case 8: reduce_rows_call<8>(rs, mask, sh, out, n16, lane); break;
       default: zero_row(out, n16, lane); break;
     }
     if (a.combined_topk_weights != nullptr && lane < k) {
@@ -301,6 +315,12 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   const uint32_t epoch = P.epoch[lr];
   const int par = epoch & 1;
   trace_mark(rv, 15);
+  __shared__ int32_t s_sh[kShTokens][kMaxRanks];
+  {
+    const int T = a.num_tokens, Tb = (T + nb - 1) / nb, tb0 = b * Tb, nt = min(T, tb0 + Tb) - tb0;
+    if (nt > 0 && nt <= kShTokens)
+      for (int i = threadIdx.x; i < nt * R; i += blockDim.x) s_sh[i / R][i % R] = a.send_head[(size_t)tb0 * R + i];
+  }
   __shared__ int32_t s_cnt[kMaxRanks][kMaxRanks];  // count[s][d]
   __shared__ int32_t s_excl[kMaxRanks];            // first row from s in my receive order
   __shared__ int32_t s_sendpre[kMaxRanks];         // where my rows start in s's staging
@@ -341,7 +361,7 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
       trace_mark(rv, 17);
     } else if (!abort) {
       trace_mark_max(rv, 21);
-      reduce_tokens(P, lr, false, s_xoff, s_woff, s_excl, s_mypre);
+      reduce_tokens(P, lr, false, s_xoff, s_woff, s_excl, s_mypre, s_sh);
       trace_mark(rv, 19);
       trace_mark_max(rv, 20);
     }
@@ -418,7 +438,7 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   trace_mark_max(rv, 21);
   if (abort) return;
 
-  reduce_tokens(P, lr, pull, s_xoff, s_woff, s_excl, s_mypre);
+  reduce_tokens(P, lr, pull, s_xoff, s_woff, s_excl, s_mypre, s_sh);
   trace_mark(rv, 19);
   trace_mark_max(rv, 20);
   if (pull) {
