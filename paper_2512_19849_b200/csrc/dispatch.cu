@@ -69,6 +69,9 @@ struct DispatchParams {
   int n_local, num_slots;
   int proxy;                    // ht_transport = CPU proxy (rows to peers go through the FIFO)
   int notify_only;              // chunked-ring transport: counts, handle and host counts only (chunked.cu moves rows)
+  int solo;                     // one rank, direct transport, T <= capacity: block 0 only runs the count
+                                // exchange (its channel is empty) and every other block derives its own
+                                // channel offset, so copies start without waiting for the plan
   int fifo_channels;
   uint64_t ht_calls[kMaxLocal];  // proxy transport: expected ht_sig[0][src] (calls so far)
   uint32_t epoch[kMaxLocal];   // per-call epoch: the tag of this call's mailbox / host words
@@ -392,8 +395,11 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   if (c == 0 && warp >= R && warp < 2 * R) post_expert_counts(P, lr, warp - R);
 
   // 1. channel-relative positions and per-(destination, channel) counts
-  const int Tc = (T + C - 1) / C;
-  const int t0 = c * Tc, nt = max(0, min(T, t0 + Tc) - t0);
+  // channel c = a contiguous token range (solo: channel 0 is empty, the
+  // tokens are spread over channels 1..C-1)
+  const int Tc = P.solo ? (T + C - 2) / (C - 1) : (T + C - 1) / C;
+  const int t0 = P.solo ? (c == 0 ? 0 : (c - 1) * Tc) : c * Tc;
+  const int nt = (P.solo && c == 0) ? 0 : max(0, min(T, t0 + Tc) - t0);
   if (warp < R) {
     const int d = warp;
     int run = 0;
@@ -414,7 +420,23 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     exchange_counts(P, lr, C, s_cnt, s_rpm, s_slot, &s_abort);
     __syncthreads();
   }
-  if (warp == 0) {
+  if (P.solo && c > 0) {
+    // my channel offset = tokens before t0 that go to rank 0 (read straight
+    // from is_token_in_rank: <= T bytes, one load round); slot and base are mine
+    __shared__ int s_before;
+    if (tid == 0) s_before = 0;
+    __syncthreads();
+    int n = 0;
+    for (int i = tid; i < t0; i += blockDim.x) n += a.is_token_in_rank[i] != 0;
+    n = __reduce_add_sync(0xffffffffu, n);
+    if (lane == 0 && n) atomicAdd(&s_before, n);
+    __syncthreads();
+    if (tid == 0) {
+      s_slotv[0] = a.recv_slot;
+      s_base[0] = 0;
+      s_chx[0] = s_before;
+    }
+  } else if (warp == 0 && !(P.solo && c == 0)) {
     const int nf = P.proxy ? 5 : 3;  // slot, row base, channel offset (+ my count, staging start)
     for (int i = lane; i < nf * R; i += 32) {
       const int d = i % R, f = i / R;
@@ -578,6 +600,11 @@ static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_a
     if (!notify_only)
       if (int e = compute_recv_layout(ctxs[i], a.hidden, a.num_topk, &P.lay)) return e;
     max_tc = std::max(max_tc, (a.num_tokens + num_channels - 1) / num_channels);
+    if (n_local == 1 && ctxs[0]->world == 1 && !P.proxy && !notify_only && num_channels >= 2 &&
+        (int64_t)a.num_tokens <= P.lay.cap_rows) {
+      P.solo = 1;
+      max_tc = std::max(max_tc, (a.num_tokens + num_channels - 2) / (num_channels - 1));
+    }
   }
   const size_t smem = sizeof(int32_t) * (size_t)max_tc * ctxs[0]->world;
   if (smem > 160 * 1024) return epb_set_error(EPB_ERR_CONFIG, "too many tokens per channel; raise num_sms");
