@@ -181,6 +181,19 @@ extern "C" int epb_open_peers(epb_t* ctx, const void* handles) {
     e = cudaMemcpy(ctx->base + probe, ctx->peer[r] + probe, 16, cudaMemcpyDefault);
     if (e == cudaSuccess) e = cudaMemcpy(ctx->peer[r] + probe + 16, ctx->base + probe + 16, 16, cudaMemcpyDefault);
     if (e != cudaSuccess) return epb_cuda_check(e, "peer mapping warm-up copy");
+    // ... and every 2 MB page of the data region (read, then write back the
+    // same bytes; nothing runs on the peer's region yet), so no copy engine
+    // meets an untouched page of the mapping while a kernel waits on it
+    const size_t stride = (size_t)2 << 20, start = epb::kRegionHeader;
+    const size_t rows = ctx->region_bytes > start ? (ctx->region_bytes - start) / stride : 0;
+    if (rows > 0) {
+      void* tmp = nullptr;
+      e = cudaMalloc(&tmp, rows * 16);
+      if (e == cudaSuccess) e = cudaMemcpy2D(tmp, 16, ctx->peer[r] + start, stride, 16, rows, cudaMemcpyDefault);
+      if (e == cudaSuccess) e = cudaMemcpy2D(ctx->peer[r] + start, stride, tmp, 16, 16, rows, cudaMemcpyDefault);
+      if (tmp) cudaFree(tmp);
+      if (e != cudaSuccess) return epb_cuda_check(e, "peer mapping page warm-up");
+    }
   }
   if (!ctx->barrier) {  // the proxies' all-peer barrier segment, named after the job's handles
     const std::string name = epb_barrier_name(handles, (size_t)ctx->world * EPB_IPC_HANDLE_BYTES);
