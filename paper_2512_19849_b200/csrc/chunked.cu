@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_dispatch_kernel(const __
   if (role == 0) {
     for (int d = grp; d < R; d += ng) {
       uint32_t sent = sc->rc_sent[0][d][l];
+      uint32_t published = sent;  // tail value last released
       char* ring = ring_at(rv.peer[d], g, 0, me, l);
       uint32_t* tail = &meta_of(rv.peer[d])->rc_tail[0][me][l];
       const int base_d = me > 0 ? a.rank_prefix_matrix[(me - 1) * R + d] : 0;
@@ -182,11 +183,17 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_dispatch_kernel(const __
             *reinterpret_cast<int32_t*>(slot + g.o_row) = base_d + shj;
           }
         }
-        // the group's stores of this chunk precede the tail (release cumulativity over the barrier)
+        // the tail advances by whole 32-token chunks (32 tokens
+        // -> one chunk write + one tail update, 33 -> two) and at the end; the
+        // group's stores precede it (release cumulativity over the barrier)
         group_sync(1 + grp, gw * 32);
         sent += (uint32_t)n;
-        if (wig == 0 && lane == 0) st_release_sys(tail, sent);
+        if (wig == 0 && lane == 0 && (sent - published >= (uint32_t)kRingChunk || w0 + kRingChunk >= t_hi)) {
+          st_release_sys(tail, sent);
+          published = sent;
+        }
       }
+      if (wig == 0 && lane == 0 && published != sent) st_release_sys(tail, sent);
       if (wig == 0 && lane == 0) sc->rc_sent[0][d][l] = sent;
     }
   } else {
