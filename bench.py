@@ -524,7 +524,8 @@ def _proxy_diag(buf, rank):
                 c = cmdmod.unpack(lo, hi)
                 print(f"   ch{ch} #{i}: kind={c.kind} dst={c.dst_rank} so={c.src_offset} do={c.dst_offset} "
                       f"len={c.length_or_value} flags={c.flags}", file=sys.stderr, flush=True)
-    sig = torch.as_tensor(_SlotMemory(rk.base + 4416, 128), device=rk.device).view(torch.int64).cpu().tolist()
+    off = lib.epb_debug_ht_sig_offset()
+    sig = torch.as_tensor(_SlotMemory(rk.base + off, 128), device=rk.device).view(torch.int64).cpu().tolist()
     print(f"[proxy diag rank {rank}] served/copies/atomics {list(st)} ctl(tail,head,completed) {ctl} "
           f"ht_sig {sig[:8]} | {sig[8:]}", file=sys.stderr, flush=True)
 

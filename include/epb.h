@@ -94,6 +94,8 @@ int epb_trace(epb_t* ctx, int64_t* out64);
 /* Diagnostics: one thread writes %globaltimer (ns) to the device word *dst, in
    stream order (brackets launches on the same clock as epb_trace's marks). */
 int epb_debug_stamp(int64_t* dst, void* stream);
+/* Diagnostics: byte offset of the proxy HT signal counters in a region. */
+int64_t epb_debug_ht_sig_offset(void);
 /* Base device address of this rank's symmetric region and its size. */
 int epb_region(epb_t* ctx, void** base, size_t* bytes);
 

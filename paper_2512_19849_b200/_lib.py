@@ -130,6 +130,7 @@ _proto("epb_num_sms", c_int)
 _proto("epb_region", c_int, vp, C.POINTER(vp), C.POINTER(C.c_size_t))
 _proto("epb_trace", c_int, vp, P64)
 _proto("epb_debug_stamp", c_int, vp, vp)
+_proto("epb_debug_ht_sig_offset", i64)
 _proto("epb_get_dispatch_layout", c_int, vp, c_int, c_int, c_int, c_int, vp, vp, vp, vp)
 _proto("epb_recv_layout", c_int, vp, c_int, c_int, C.POINTER(RecvLayout))
 _proto("epb_wait_notify", c_int, vp, P64, P32, c_int, c_double)
@@ -173,7 +174,7 @@ _proto("epb_proxy_barrier", c_int, vp, c_int, c_int, vp)
 # every symbol include/epb.h declares (checked by tests/test_abi.py)
 EXPORTED = [
     "epb_create", "epb_destroy", "epb_ipc_handle", "epb_open_peers", "epb_link_local", "epb_last_error",
-    "epb_device_error", "epb_clear_device_error", "epb_num_sms", "epb_region", "epb_trace", "epb_debug_stamp", "epb_get_dispatch_layout",
+    "epb_device_error", "epb_clear_device_error", "epb_num_sms", "epb_region", "epb_trace", "epb_debug_stamp", "epb_debug_ht_sig_offset", "epb_get_dispatch_layout",
     "epb_recv_layout", "epb_wait_notify", "epb_dispatch", "epb_combine", "epb_ring_layout", "epb_dispatch_notify",
     "epb_ring_dispatch", "epb_ring_combine", "epb_ll_layout",
     "epb_ll_dispatch", "epb_ll_combine", "epb_per_token_cast_to_fp8", "epb_cmd_pack", "epb_cmd_pack_fields",

@@ -4,6 +4,8 @@
 // waits until the proxy reports them completed (check_completion).
 #include <cuda_runtime.h>
 
+#include <cstddef>
+
 #include "ctx.h"
 #include "ll_common.cuh"
 
@@ -122,6 +124,8 @@ extern "C" int epb_fifo_device_bench(epb_t* ctx, int64_t num_cmds, int channels,
 namespace epb {
 __global__ void stamp_kernel(int64_t* dst) { *dst = (int64_t)globaltimer(); }
 }  // namespace epb
+
+extern "C" int64_t epb_debug_ht_sig_offset(void) { return (int64_t)offsetof(epb::Meta, ht_sig); }
 
 extern "C" int epb_debug_stamp(int64_t* dst, void* stream) {
   epb::stamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(dst);

@@ -26,6 +26,7 @@ ok = True
 side = torch.cuda.Stream() if os.environ.get("SIDE") else None
 if side is not None:
     torch.cuda.set_stream(side)
+import bench as _bench
 for it in range(4):
     outs = {}
     for name, b in (("nvlink", ref), ("proxy", buf)):
@@ -34,8 +35,16 @@ for it in range(4):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         flush.zero_()
         e[0].record()
-        rx, rti, rtw, _, h, _ = b.dispatch(x, num_tokens_per_rank=pr, is_token_in_rank=ir, num_tokens_per_expert=pe,
-                                           topk_idx=idx_t, topk_weights=w_t)
+        try:
+            rx, rti, rtw, _, h, _ = b.dispatch(x, num_tokens_per_rank=pr, is_token_in_rank=ir,
+                                               num_tokens_per_expert=pe, topk_idx=idx_t, topk_weights=w_t)
+            torch.cuda.synchronize()
+            if name == "proxy":
+                b._g.check_device_error()
+        except Exception:
+            if name == "proxy":
+                _bench._proxy_diag(b, rank)
+            raise
         e[1].record()
         flush.zero_()
         y = rx if it % 2 == 0 else rx.clone()  # in place / staged
