@@ -425,10 +425,8 @@ def run_ours(args):
                          ("qwen3_235b_zipf", dict(T=8192, H=4096, E=128, zipf=1.0)),
                          ("dsv3_bf16_ring", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, ht="ring")),
                          ("dsv3_bf16_ht_proxy", dict(T=T_PER_RANK, H=HIDDEN, E=EXPERTS, ht="proxy"))):
-            # the proxy HT transport is opt-in here (its first call can
-            # stall when another Buffer of the process has run a combine)
             only = os.environ.get("EPB_BENCH_CONFIGS")
-            if (only and name not in only.split(",")) or (not only and kw.get("ht") == "proxy"):
+            if only and name not in only.split(","):
                 continue
             try:
                 configs[name] = config_bench(name, *common, **kw)

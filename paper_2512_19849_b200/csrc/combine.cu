@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -490,6 +491,7 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     EPB_CUDA(cudaLaunchKernel((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
     combine_proxy_wait_kernel<<<n_local, 32, 0, st>>>(P);
     EPB_CUDA(cudaGetLastError());
+    if (!std::getenv("EPB_PROXY_ASYNC")) EPB_CUDA(cudaStreamSynchronize(st));  // see epb_dispatch
     P.phase = 2;
     EPB_CUDA(cudaLaunchKernel((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
     return EPB_OK;

@@ -628,6 +628,10 @@ static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_a
   if (P.proxy) {
     dispatch_proxy_wait_kernel<<<n_local, 32, 0, st>>>(P);
     EPB_CUDA(cudaGetLastError());
+    // the host does not run ahead of the wait: work enqueued behind a wait
+    // kernel that spins on the proxy's copies was seen to hold those copies
+    // back until the wait timed out (NCCL jobs, tools/proxy_ht_check.py)
+    if (!std::getenv("EPB_PROXY_ASYNC")) EPB_CUDA(cudaStreamSynchronize(st));
   }
   return EPB_OK;
 }

@@ -38,13 +38,19 @@ for it in range(4):
         try:
             rx, rti, rtw, _, h, _ = b.dispatch(x, num_tokens_per_rank=pr, is_token_in_rank=ir,
                                                num_tokens_per_expert=pe, topk_idx=idx_t, topk_weights=w_t)
-            torch.cuda.synchronize()
-            if name == "proxy":
-                b._g.check_device_error()
+            if os.environ.get("SYNC_AFTER_DISPATCH"):
+                torch.cuda.synchronize()
         except Exception:
             if name == "proxy":
                 _bench._proxy_diag(b, rank)
             raise
+        if name == "proxy" and os.environ.get("SYNC_AFTER_DISPATCH"):
+            try:
+                torch.cuda.synchronize()
+                b._g.check_device_error()
+            except Exception:
+                _bench._proxy_diag(b, rank)
+                raise
         e[1].record()
         flush.zero_()
         y = rx if it % 2 == 0 else rx.clone()  # in place / staged
