@@ -80,6 +80,7 @@ def _emulated_dispatch(torch, R, Ts, H, E, k, seed, fp8=False, mask=0.0, zipf=0.
 
 @pytest.mark.parametrize("R,Ts,H,E,k,mask,sms,ht", [
     (1, [300], 1024, 16, 4, 0.0, None, "nvlink"),
+    (1, [777], 2048, 16, 4, 0.3, None, "nvlink"),  # single-rank path with fully masked tokens
     (2, [257, 64], 2048, 32, 4, 0.0, 7, "nvlink"),
     (4, [128, 128, 128, 128], 1024, 32, 2, 0.0, None, "nvlink"),
     (4, [0, 333, 1, 50], 7168, 64, 8, 0.2, 20, "nvlink"),
@@ -213,14 +214,17 @@ def test_capacity_overflow_raises_config_error(torch):
     grp.destroy()
 
 
-def test_buffer_single_rank_deepseek_shape(torch):
-    """Buffer at N=1 (EP=1) on the DeepSeek-V3 shape: recv_x == x, combine(dispatch(x)) == x."""
-    from paper_2512_19849_b200 import Buffer, nvl_bytes_hint
+@pytest.mark.parametrize("ht", ["nvlink", "ring"])
+def test_buffer_single_rank_deepseek_shape(torch, ht):
+    """Buffer at N=1 (EP=1) on the DeepSeek-V3 shape: recv_x == x, combine(dispatch(x)) == x
+    (the single-rank dispatch path, and the chunked-ring transport)."""
+    from paper_2512_19849_b200 import Buffer, nvl_bytes_hint, ring_nvl_bytes
     T, H, E, k = 4096, 7168, 256, 8
     g = np.random.default_rng(42)
     idx, w = make_routing(g, T, E, k)
     x = to_dev_bf16(bf16_random(g, (T, H)))
-    buf = Buffer(None, nvl_bytes_hint(T, H, 1, k))
+    nvl = ring_nvl_bytes(H, 1, k) if ht == "ring" else nvl_bytes_hint(T, H, 1, k)
+    buf = Buffer(None, nvl, ht_transport=ht)
     topk = torch.from_numpy(idx).cuda()
     wt = torch.from_numpy(w).cuda()
     per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(topk, E)
