@@ -69,6 +69,8 @@ struct DispatchParams {
   int n_local, num_slots;
   int proxy;                    // ht_transport = CPU proxy (rows to peers go through the FIFO)
   int notify_only;              // chunked-ring transport: counts, handle and host counts only (chunked.cu moves rows)
+  int perblock;                 // R > 1, direct transport: blocks other than 0 read the peers' mailbox
+                                // words and derive their channel offsets themselves (no block-0 plan hop)
   int solo;                     // one rank, direct transport, T <= capacity: block 0 only runs the count
                                 // exchange (its channel is empty) and every other block derives its own
                                 // channel offset, so copies start without waiting for the plan
@@ -420,7 +422,85 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     exchange_counts(P, lr, C, s_cnt, s_rpm, s_slot, &s_abort);
     __syncthreads();
   }
-  if (P.solo && c > 0) {
+  if (P.perblock && c > 0) {
+    // my channel's offset in my run to each d: tokens before t0 that go to d
+    __shared__ int s_before[kMaxRanks];
+    if (tid < R) s_before[tid] = 0;
+    __syncthreads();
+    int n[kMaxRanks];
+#pragma unroll
+    for (int d = 0; d < kMaxRanks; ++d) n[d] = 0;
+    for (int t = tid; t < t0; t += blockDim.x) {
+      uint64_t bits = 0;  // the token's R bool bytes (one aligned load for R = 2, 4, 8)
+      const uint8_t* row = a.is_token_in_rank + (size_t)t * R;
+      if (R == 8) bits = *reinterpret_cast<const uint64_t*>(row);
+      else if (R == 4) bits = *reinterpret_cast<const uint32_t*>(row);
+      else if (R == 2) bits = *reinterpret_cast<const uint16_t*>(row);
+      else
+        for (int d = 0; d < R; ++d) bits |= (uint64_t)row[d] << (8 * d);
+#pragma unroll
+      for (int d = 0; d < kMaxRanks; ++d) n[d] += ((bits >> (8 * d)) & 0xff) != 0;
+    }
+#pragma unroll
+    for (int d = 0; d < kMaxRanks; ++d) {
+      if (d >= R) break;
+      const int v = __reduce_add_sync(0xffffffffu, n[d]);
+      if (lane == 0 && v) atomicAdd(&s_before[d], v);
+    }
+    // warp 0: every source's totals and every destination's slot from my
+    // mailbox (the words block 0 of each rank posts), then the same
+    // capacity checks block 0 makes (all ranks see the same matrix)
+    if (warp == 0) {
+      constexpr int kPer = (kMaxRanks * (kMaxRanks + 1) + 31) / 32;
+      const Meta* my = meta_of(rv.base);
+      const int par = epoch & 1;
+      uint64_t v[kPer];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int i = lane + 32 * j, s2 = i / (R + 1), f = i % (R + 1);
+        v[j] = i < R * (R + 1) ? ld_relaxed_sys(f < R ? &my->mbox[par][s2].counts_per_rank[f] : &my->mbox[par][s2].slot)
+                               : tagged(0, epoch);
+      }
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int i = lane + 32 * j, s2 = i / (R + 1), f = i % (R + 1);
+        if (i < R * (R + 1)) {
+          const uint64_t* w = f < R ? &my->mbox[par][s2].counts_per_rank[f] : &my->mbox[par][s2].slot;
+          const uint32_t x = (uint32_t)v[j] == epoch ? (uint32_t)(v[j] >> 32) : wait_tagged(rv, w, epoch, 0x1a0 + s2, 64);
+          if (x == kNotifyAbort) s_abort = EPB_ERR_DEADLOCK;
+          if (f < R) s_rpm[s2][f] = (int)x;
+          else s_slot[s2] = (int)x;
+        }
+      }
+      __syncwarp();
+      if (lane < R) {  // inclusive prefix over source rank, column d
+        int run = 0;
+        for (int s2 = 0; s2 < R; ++s2) {
+          run += s_rpm[s2][lane];
+          s_rpm[s2][lane] = run;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int64_t cap = P.lay.cap_rows;
+        bool bad = false;
+        for (int d = 0; d < R; ++d) bad |= s_slot[d] < 0 || s_slot[d] >= P.num_slots || s_rpm[R - 1][d] > cap;
+        for (int s2 = 0; s2 < R; ++s2) {
+          int sent = 0;
+          for (int d = 0; d < R; ++d) sent += s_rpm[s2][d] - (s2 > 0 ? s_rpm[s2 - 1][d] : 0);
+          bad |= sent > cap;
+        }
+        if (bad) s_abort = EPB_ERR_CONFIG;  // block 0 reports it; this block just does not copy
+      }
+    }
+    __syncthreads();
+    if (tid < R) {
+      const int d = tid;
+      s_slotv[d] = s_slot[d];
+      s_base[d] = me > 0 ? s_rpm[me - 1][d] : 0;
+      s_chx[d] = s_before[d];
+    }
+  } else if (P.solo && c > 0) {
     // my channel offset = tokens before t0 that go to rank 0 (read straight
     // from is_token_in_rank: <= T bytes, one load round); slot and base are mine
     __shared__ int s_before;
@@ -436,7 +516,7 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
       s_base[0] = 0;
       s_chx[0] = s_before;
     }
-  } else if (warp == 0 && !(P.solo && c == 0)) {
+  } else if (warp == 0 && !(P.solo && c == 0)) {  // block 0, and every block of the proxy transport
     const int nf = P.proxy ? 5 : 3;  // slot, row base, channel offset (+ my count, staging start)
     for (int i = lane; i < nf * R; i += 32) {
       const int d = i % R, f = i / R;
@@ -600,6 +680,7 @@ static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_a
     if (!notify_only)
       if (int e = compute_recv_layout(ctxs[i], a.hidden, a.num_topk, &P.lay)) return e;
     max_tc = std::max(max_tc, (a.num_tokens + num_channels - 1) / num_channels);
+    if (ctxs[0]->world > 1 && !P.proxy && !notify_only && !std::getenv("EPB_PLAN_HOP")) P.perblock = 1;
     if (n_local == 1 && ctxs[0]->world == 1 && !P.proxy && !notify_only && num_channels >= 2 &&
         (int64_t)a.num_tokens <= P.lay.cap_rows) {
       P.solo = 1;
