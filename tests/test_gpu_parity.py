@@ -211,6 +211,14 @@ def test_capacity_overflow_raises_config_error(torch):
     x = [torch.zeros(4096, 7168, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
     with pytest.raises(ConfigError):
         grp.dispatch(x, [l[3] for l in lay], [l[2] for l in lay], topk_dev, None)
+    # the group stays usable: counters and epochs are in step after the abort
+    from paper_2512_19849_b200.errors import EpsimError
+    try:
+        grp.check_device_error()
+    except EpsimError:
+        pass
+    _, xs, idxs2, ws, _, _, _, res = _emulated_dispatch(torch, 2, [64, 32], 1024, 16, 4, seed=3, grp=grp)
+    _check_dispatch_combine(torch, grp, 2, 16, xs, idxs2, ws, res)
     grp.destroy()
 
 
