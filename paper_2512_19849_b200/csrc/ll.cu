@@ -3,10 +3,11 @@
 //   ll_dispatch : one message per (token, expert), no dedup (SPEC.md:426-434,
 //                 :463), fused FP8 e4m3 quantisation per 128 channels,
 //                 deterministic slots (rank of the token among the source's
-//                 tokens for that expert), one completion signal per source
-//                 (the LL fence of PAPER.md:343-346 / kernels.py:187-248
-//                 collapses to "all X writes, then the count" because NVLink
-//                 stores + release/acquire are ordered).
+//                 tokens for that expert), completion counted per sender
+//                 block (the LL fence of PAPER.md:343-346 / kernels.py:187-248
+//                 collapses to "all X writes, then the count": each block's
+//                 red.release.sys covers its rows, block 0's also the count
+//                 header, and the receiver acquires the per-source counter).
 //   ll_combine  : expert outputs pushed back to the source, weighted top-k
 //                 reduce in fp32 in ascending top-k order.
 //
