@@ -68,7 +68,29 @@ int epb_max_active_blocks(const void* func, int threads, size_t smem) {
 
 // Raises the kernel's dynamic shared-memory limit to `smem` (static shared
 // memory counts against the default 48 KB, so any nonzero request may need it).
+// One shared-memory carveout for every kernel of the normal-mode step
+// (EPB_CARVEOUT, percent; negative = the driver's per-kernel choice).  With
+// the driver's choice the N=1 step (layout, dispatch, combine back to back)
+// took 70-73 us on B200; with the maximum shared carveout for all three it
+// took 63 us, although dispatch and combine alone got ~1 us slower each
+// (profiles/r01d_summary.md).
+void epb_set_carveout(const void* func) {
+  static const int pct = [] {
+    const char* s = std::getenv("EPB_CARVEOUT");
+    return s ? std::atoi(s) : 100;
+  }();
+  if (pct < 0) return;
+  static std::vector<const void*> done;
+  std::lock_guard<std::mutex> g(g_cfg_mu);
+  for (const void* f : done)
+    if (f == func) return;
+  cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaGetLastError();
+  done.push_back(func);
+}
+
 cudaError_t epb_ensure_smem(const void* func, size_t smem) {
+  epb_set_carveout(func);
   if (smem == 0) return cudaSuccess;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -485,6 +485,7 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     P.a[i] = a;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  epb_set_carveout((const void*)combine_kernel);
   void* kargs[] = {&P};
   if (P.proxy) {  // stage + push | wait for the peers' rows | reduce
     P.phase = 1;

@@ -248,11 +248,16 @@ extern "C" int epb_get_dispatch_layout(const int64_t* topk_idx, int num_tokens, 
       cudaError_t e = cudaSuccess;
       if (cluster_ok < 0) {
         e = cudaFuncSetAttribute((const void*)layout_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e == cudaSuccess)
-          e = cudaFuncSetAttribute((const void*)layout_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   200 * 1024);
       }
+      // the opt-in limit tracks the real need: a 200 KB limit made the driver
+      // give this kernel a different L1/shared split from the dispatch and
+      // combine kernels around it, and the SM reconfigured between them
+      if (e == cudaSuccess && !std::getenv("EPB_LAYOUT_SMEM_MAX")) e = epb_ensure_smem((const void*)layout_cluster_kernel, csmem);
+      else if (e == cudaSuccess && cluster_ok < 0)
+        e = cudaFuncSetAttribute((const void*)layout_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024);
       if (e == cudaSuccess) {
+        epb_set_carveout((const void*)layout_cluster_kernel);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(kClusterBlocks);
         cfg.blockDim = dim3(kClusterThreads);
