@@ -74,19 +74,29 @@ int epb_max_active_blocks(const void* func, int threads, size_t smem) {
 // took 70-73 us on B200; with the maximum shared carveout for all three it
 // took 63 us, although dispatch and combine alone got ~1 us slower each
 // (profiles/r01d_summary.md).
-void epb_set_carveout(const void* func) {
+void epb_set_carveout(const void* func, bool enable) {
   static const int pct = [] {
     const char* s = std::getenv("EPB_CARVEOUT");
     return s ? std::atoi(s) : 100;
   }();
-  if (pct < 0) return;
-  static std::vector<const void*> done;
+  const int want = enable ? pct : -1;  // -1 = cudaSharedmemCarveoutDefault
+  static std::vector<std::pair<const void*, int>> done;
   std::lock_guard<std::mutex> g(g_cfg_mu);
-  for (const void* f : done)
-    if (f == func) return;
-  cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  for (auto& d : done)
+    if (d.first == func) {
+      if (d.second == want) return;
+      d.second = want;
+      cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, want);
+      cudaGetLastError();
+      return;
+    }
+  if (want < 0) {  // never changed: already the driver's choice
+    done.emplace_back(func, want);
+    return;
+  }
+  cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, want);
   cudaGetLastError();
-  done.push_back(func);
+  done.emplace_back(func, want);
 }
 
 cudaError_t epb_ensure_smem(const void* func, size_t smem) {

@@ -623,6 +623,7 @@ extern "C" int epb_ll_combine(epb_t* const* ctxs, int n_local, const epb_ll_comb
     P.rv[i] = c->view();
     P.a[i] = args[i];
   }
+  epb_set_carveout((const void*)ll_combine_kernel);  // same split as ll_dispatch_kernel
   const int nb = ll_blocks(ctxs, n_local, num_sms, (const void*)ll_combine_kernel, 0, 1);
   if (nb == 0) return epb_set_error(EPB_ERR_CONFIG, "LL combine: grid no longer co-resident");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
