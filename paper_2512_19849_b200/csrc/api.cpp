@@ -68,12 +68,9 @@ int epb_max_active_blocks(const void* func, int threads, size_t smem) {
 
 // Raises the kernel's dynamic shared-memory limit to `smem` (static shared
 // memory counts against the default 48 KB, so any nonzero request may need it).
-// One shared-memory carveout for every kernel of the normal-mode step
-// (EPB_CARVEOUT, percent; negative = the driver's per-kernel choice).  With
-// the driver's choice the N=1 step (layout, dispatch, combine back to back)
-// took 70-73 us on B200; with the maximum shared carveout for all three it
-// took 63 us, although dispatch and combine alone got ~1 us slower each
-// (profiles/r01d_summary.md).
+// Shared-memory carveout for the path's kernels (EPB_CARVEOUT, percent,
+// default 100 = maximum shared; negative = the driver's per-kernel choice).
+// Set for the dispatch, layout and LL kernels; see dispatch_launch.
 void epb_set_carveout(const void* func, bool enable) {
   static const int pct = [] {
     const char* s = std::getenv("EPB_CARVEOUT");
@@ -99,8 +96,12 @@ void epb_set_carveout(const void* func, bool enable) {
   done.emplace_back(func, want);
 }
 
+bool epb_carveout_skip(const char* name) {
+  const char* s = std::getenv("EPB_CARVEOUT_SKIP");  // e.g. "dispatch,combine" (measurement only)
+  return s && std::strstr(s, name);
+}
+
 cudaError_t epb_ensure_smem(const void* func, size_t smem) {
-  epb_set_carveout(func);
   if (smem == 0) return cudaSuccess;
   int dev = 0;
   cudaGetDevice(&dev);

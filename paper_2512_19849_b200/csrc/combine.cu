@@ -471,10 +471,6 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     if (P.proxy && (ctxs[i]->cfg.fifo_channels <= 0 || !ctxs[i]->proxy || ctxs[i]->cfg.ht_transport != EPB_HT_PROXY))
       return epb_set_error(EPB_ERR_CONFIG, "ht_transport=proxy needs FIFO channels and a running proxy on every rank");
   int nb = std::max(1, num_sms / n_local);
-  // max shared carveout at EP=1 only: it removes the SM reconfiguration
-  // between the step's kernels (N=1 step 70 -> 63 us), but at EP=2 the pull
-  // reduce lost 5 us to the smaller L1 (profiles/r01d_summary.md)
-  epb_set_carveout((const void*)combine_kernel, ctxs[0]->world == 1);  // before the occupancy query
   const int max_active = epb_max_active_blocks((const void*)combine_kernel, kCombineThreads, 0);
   nb = std::min(nb, std::max(1, max_active * ctxs[0]->num_sms / n_local));
   for (int i = 0; i < n_local; ++i) {

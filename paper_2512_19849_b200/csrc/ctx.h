@@ -63,6 +63,7 @@ cudaError_t epb_launch_grid_sync(const void* func, dim3 grid, dim3 block, void**
 int epb_max_active_blocks(const void* func, int threads, size_t smem);
 cudaError_t epb_ensure_smem(const void* func, size_t smem);
 void epb_set_carveout(const void* func, bool enable = true);
+bool epb_carveout_skip(const char* name);
 
 // name of the job-wide barrier segment (barrier.cpp)
 std::string epb_barrier_name(const void* bytes, size_t n);

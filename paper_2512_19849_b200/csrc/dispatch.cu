@@ -689,6 +689,11 @@ static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_a
   }
   const size_t smem = sizeof(int32_t) * (size_t)max_tc * ctxs[0]->world;
   if (smem > 160 * 1024) return epb_set_error(EPB_ERR_CONFIG, "too many tokens per channel; raise num_sms");
+  // max shared carveout: the N=1 step (layout, dispatch, combine back to back)
+  // took 70 us with the driver's choice and 63 us with this, although the
+  // dispatch alone is ~2 us slower; the gain is in the gap after the dispatch
+  // (profiles/r01d_summary.md).  The combine keeps the driver's choice.
+  epb_set_carveout((const void*)dispatch_kernel, !epb_carveout_skip("dispatch"));
   EPB_CUDA(epb_ensure_smem((const void*)dispatch_kernel, smem));
   const int max_active = epb_max_active_blocks((const void*)dispatch_kernel, kDispatchThreads, smem);
   if ((int64_t)num_channels * n_local > (int64_t)max_active * ctxs[0]->num_sms)

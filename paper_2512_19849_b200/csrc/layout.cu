@@ -257,7 +257,7 @@ extern "C" int epb_get_dispatch_layout(const int64_t* topk_idx, int num_tokens, 
         e = cudaFuncSetAttribute((const void*)layout_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  200 * 1024);
       if (e == cudaSuccess) {
-        epb_set_carveout((const void*)layout_cluster_kernel);
+        epb_set_carveout((const void*)layout_cluster_kernel, !epb_carveout_skip("layout"));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(kClusterBlocks);
         cfg.blockDim = dim3(kClusterThreads);
@@ -288,6 +288,7 @@ extern "C" int epb_get_dispatch_layout(const int64_t* topk_idx, int num_tokens, 
   }();
   const size_t smem = sizeof(int64_t) * threads * num_topk + sizeof(int32_t) * (num_experts + num_ranks);
   if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "num_experts too large for layout kernel");
+  epb_set_carveout((const void*)layout_kernel, !epb_carveout_skip("layout"));
   EPB_CUDA(epb_ensure_smem((const void*)layout_kernel, smem));
   const int per_sm = std::max(1, epb_max_active_blocks((const void*)layout_kernel, threads, smem));
   int blocks = std::max(1, (num_tokens + threads - 1) / threads);

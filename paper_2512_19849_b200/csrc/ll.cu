@@ -594,6 +594,7 @@ extern "C" int epb_ll_dispatch(epb_t* const* ctxs, int n_local, const epb_ll_dis
   const size_t smem_recv = (size_t)(3 * P.g.R * P.g.L + P.g.L + 1) * 4;
   const size_t smem = std::max(smem_send, smem_recv);
   if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "LL dispatch shape needs too much shared memory");
+  epb_set_carveout((const void*)ll_dispatch_kernel);
   EPB_CUDA(epb_ensure_smem((const void*)ll_dispatch_kernel, smem));
   const int nb = ll_blocks(ctxs, n_local, num_sms, (const void*)ll_dispatch_kernel, smem, 0);
   if (nb == 0) return epb_set_error(EPB_ERR_CONFIG, "LL dispatch: this shape no longer fits the context's pinned grid");
