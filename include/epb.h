@@ -213,6 +213,8 @@ typedef struct {
   int64_t* recv_topk_idx;     /* [N_recv, num_topk] or NULL                    */
   float* recv_topk_weights;   /* [N_recv, num_topk] or NULL                    */
   int32_t* recv_src_idx;      /* [N_recv]                                      */
+  int num_recv;               /* N_recv (from epb_wait_notify): receive rows are
+                                 bounds-checked against it                     */
 } epb_ring_dispatch_args_t;
 
 int epb_ring_dispatch(epb_t* const* ctxs, int n_local, const epb_ring_dispatch_args_t* args, int lanes,

@@ -79,7 +79,7 @@ class RingDispatchArgs(C.Structure):
                 ("topk_idx", vp), ("topk_weights", vp), ("num_topk", C.c_int), ("num_tokens", C.c_int),
                 ("num_experts", C.c_int), ("rank_prefix_matrix", vp), ("recv_channel_prefix_matrix", vp),
                 ("send_head", vp), ("num_channels", C.c_int), ("recv_x", vp), ("recv_x_scales", vp),
-                ("recv_topk_idx", vp), ("recv_topk_weights", vp), ("recv_src_idx", vp)]
+                ("recv_topk_idx", vp), ("recv_topk_weights", vp), ("recv_src_idx", vp), ("num_recv", C.c_int)]
 
 
 class RingCombineArgs(C.Structure):

@@ -126,8 +126,8 @@ def ring_nvl_bytes(hidden: int, num_ranks: int, num_topk: int = 8, lanes: int = 
     S = hidden // 128
     o_sc = up(2 * hidden, 16)
     o_ti = up(o_sc + 4 * S, 8)
-    disp = up(o_ti + 12 * num_topk + 8, 16)
-    comb = up(2 * hidden + 4 * num_topk, 16)
+    disp = up(o_ti + 12 * num_topk + 12, 16)  # ... | src idx | receive row | canary
+    comb = up(2 * hidden + 4 * num_topk + 4, 16)  # row | weights | canary
     return num_ranks * lanes * ring_tokens * (disp + comb)
 
 

@@ -109,6 +109,7 @@ def ring_dispatch(ranks, xs, x_scales, in_ranks, per_experts, topk_idxs, topk_ws
         r.send_head, r.num_channels = a.send_head, Cn
         r.recv_x, r.recv_x_scales = recv_x.data_ptr(), _ptr(recv_sc)
         r.recv_topk_idx, r.recv_topk_weights, r.recv_src_idx = _ptr(recv_ti), _ptr(recv_tw), recv_src.data_ptr()
+        r.num_recv = N
         T = a.num_tokens
         rpm = hbuf[: R * R].view(R, R)
         cpm = hbuf[R * R: R * R + R * Cn].view(R, Cn)

@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -43,8 +44,12 @@ constexpr int kRingUnroll = 7;     // 16-byte words per lane in flight per row p
 struct RingGeom {
   int lanes, ring_tokens;
   int64_t disp_slot, comb_slot, disp_off, comb_off;
-  // dispatch slot fields: row | scales | topk idx | topk weights | src idx | receive row
-  int64_t o_sc, o_ti, o_tw, o_src, o_row;
+  // dispatch slot fields: row | scales | topk idx | topk weights | src idx | receive row | canary
+  int64_t o_sc, o_ti, o_tw, o_src, o_row, o_can;
+  int64_t comb_can;  // combine slot: row | weights | canary
+  // test hook (EPB_RING_UNSAFE_NO_CREDIT=1): the sender skips the credit wait,
+  // so it overruns unread slots and the canaries must catch it
+  int no_credit;
 };
 
 struct RingDispatchParams {
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_dispatch_kernel(const __
         const unsigned b = __ballot_sync(0xffffffffu, sh >= 0);
         const int n = __popc(b);
         if (n == 0) continue;
-        if (wig == 0 && lane == 0) wait_credit(rv, &my->rc_head[0][d][l], sent, n, RT, 0x900 + d);
+        if (wig == 0 && lane == 0 && !g.no_credit) wait_credit(rv, &my->rc_head[0][d][l], sent, n, RT, 0x900 + d);
         group_sync(1 + grp, gw * 32);
         for (int j = wig; j < n; j += gw) {
           const int tj = __fns(b, 0, j + 1);
@@ -181,6 +186,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_dispatch_kernel(const __
           if (lane == 0) {
             *reinterpret_cast<int32_t*>(slot + g.o_src) = tt;
             *reinterpret_cast<int32_t*>(slot + g.o_row) = base_d + shj;
+            // canary: the slot's cumulative sequence number in this ring (SPEC.md:470,
+            // :477 "canary word per slot"); a slot overwritten before it was read
+            // carries a sequence number RT (or more) ahead of what the receiver expects
+            *reinterpret_cast<uint32_t*>(slot + g.o_can) = sent + (uint32_t)j;
           }
         }
         // the tail advances by whole 32-token chunks (32 tokens
@@ -204,6 +213,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_dispatch_kernel(const __
       const char* ring = ring_at(rv.base, g, 0, s, l);
       uint32_t* head = &meta_of(rv.peer[s])->rc_head[0][me][l];
       int done = 0;
+      if (g.no_credit && wig == 0 && lane == 0) {  // test hook: let the unthrottled sender lap the ring
+        const uint64_t t_hold = globaltimer();
+        while (globaltimer() - t_hold < 200000) __nanosleep(1000);
+      }
       while (done < n_exp) {
         if (wig == 0 && lane == 0) {
           uint64_t t0 = 0;
@@ -215,18 +228,37 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_dispatch_kernel(const __
               if (t0 == 0) t0 = now;
               else if (now - t0 > rv.timeout_ns) {
                 report_error(rv, EPB_ERR_DEADLOCK, 0x940 + s);
-                avail = n_exp - done;  // give up: drain garbage rather than hang
+                avail = -1;  // give up on this ring: nothing it holds is trusted
                 break;
               }
             }
           }
-          s_m[grp] = (uint32_t)min(avail, n_exp - done);
+          s_m[grp] = avail < 0 ? 0xffffffffu : (uint32_t)min(avail, n_exp - done);
         }
         group_sync(1 + grp, gw * 32);
+        if (s_m[grp] == 0xffffffffu) {  // timed out: skip the copy, release the credit, move on
+          done = n_exp;
+          if (wig == 0 && lane == 0) st_release_sys(head, recvd + (uint32_t)done);
+          break;
+        }
         const int m = (int)s_m[grp];
         for (int j = wig; j < m; j += gw) {
-          const char* slot = ring + (int64_t)((recvd + (uint32_t)(done + j)) & (uint32_t)(RT - 1)) * g.disp_slot;
-          const int row = __shfl_sync(0xffffffffu, lane == 0 ? __ldcg(reinterpret_cast<const int32_t*>(slot + g.o_row)) : 0, 0);
+          const uint32_t seq = recvd + (uint32_t)(done + j);
+          const char* slot = ring + (int64_t)(seq & (uint32_t)(RT - 1)) * g.disp_slot;
+          int row = 0, bad = 0;
+          if (lane == 0) {
+            row = __ldcg(reinterpret_cast<const int32_t*>(slot + g.o_row));
+            const uint32_t can = __ldcg(reinterpret_cast<const uint32_t*>(slot + g.o_can));
+            if (can != seq) {  // an unread slot was overwritten (or never written)
+              report_error(rv, EPB_ERR_INVARIANT, ((int64_t)0x9a0 << 40) | ((int64_t)s << 32) | can);
+              bad = 1;
+            } else if (row < 0 || row >= a.num_recv) {
+              report_error(rv, EPB_ERR_FAULT, ((int64_t)0x9b0 << 40) | (uint32_t)row);
+              bad = 1;
+            }
+          }
+          if (__shfl_sync(0xffffffffu, bad, 0)) continue;
+          row = __shfl_sync(0xffffffffu, row, 0);
           copy_row<false>(reinterpret_cast<const int4*>(slot),
                           reinterpret_cast<int4*>(static_cast<char*>(a.recv_x) + (size_t)row * row_bytes), n16, lane);
           if (a.recv_x_scales != nullptr)
@@ -239,6 +271,13 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_dispatch_kernel(const __
               a.recv_topk_weights[(size_t)row * k + lane] = __ldcg(reinterpret_cast<const float*>(slot + g.o_tw) + lane);
           }
           if (lane == 0) a.recv_src_idx[row] = __ldcg(reinterpret_cast<const int32_t*>(slot + g.o_src));
+          // the row's stores consumed every lane's loads; the canary must still
+          // hold this slot's sequence number (no overwrite while it was read)
+          __syncwarp();
+          if (lane == 0) {
+            const uint32_t can = __ldcg(reinterpret_cast<const uint32_t*>(slot + g.o_can));
+            if (can != seq) report_error(rv, EPB_ERR_INVARIANT, ((int64_t)0x9a1 << 40) | ((int64_t)s << 32) | can);
+          }
         }
         // every read of these slots is done before the credit goes back
         group_sync(1 + grp, gw * 32);
@@ -284,7 +323,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_combine_kernel(const __g
       uint32_t* tail = &meta_of(rv.peer[s])->rc_tail[1][me][l];
       for (int w0 = 0; w0 < n_rows; w0 += kRingChunk) {
         const int n = min(kRingChunk, n_rows - w0);
-        if (wig == 0 && lane == 0) wait_credit(rv, &my->rc_head[1][s][l], sent, n, RT, 0x980 + s);
+        if (wig == 0 && lane == 0 && !g.no_credit) wait_credit(rv, &my->rc_head[1][s][l], sent, n, RT, 0x980 + s);
         group_sync(1 + grp, gw * 32);
         for (int j = wig; j < n; j += gw) {
           const int64_t row = j0 + w0 + j;
@@ -294,6 +333,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_combine_kernel(const __g
           if (lane < k)
             reinterpret_cast<float*>(slot + row_bytes)[lane] =
                 a.topk_weights != nullptr ? a.topk_weights[row * k + lane] : 0.0f;
+          if (lane == 0) *reinterpret_cast<uint32_t*>(slot + g.comb_can) = sent + (uint32_t)j;  // canary
         }
         group_sync(1 + grp, gw * 32);
         sent += (uint32_t)n;
@@ -346,7 +386,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_combine_kernel(const __g
         const uint32_t b = s_bits[d];
         if (!((b >> tt) & 1u)) continue;
         const uint32_t idx = s_pos[d] + (uint32_t)__popc(b & ((1u << tt) - 1u));
-        src[nv++] = ring_at(rv.base, g, 1, d, l) + (int64_t)(idx & (uint32_t)(RT - 1)) * g.comb_slot;
+        src[nv] = ring_at(rv.base, g, 1, d, l) + (int64_t)(idx & (uint32_t)(RT - 1)) * g.comb_slot;
+        if (lane == 0) {
+          const uint32_t can = __ldcg(reinterpret_cast<const uint32_t*>(src[nv] + g.comb_can));
+          if (can != idx) report_error(rv, EPB_ERR_INVARIANT, ((int64_t)0x9c8 << 40) | ((int64_t)d << 32) | can);
+        }
+        ++nv;
       }
       int4* out = reinterpret_cast<int4*>(static_cast<char*>(a.combined_x) + (size_t)t * row_bytes);
       for (int i = lane; i < n16; i += 32) {
@@ -408,8 +453,12 @@ static int ring_geometry(const epb_ctx* c, int hidden, int k, int lanes, int n_l
   g->o_tw = g->o_ti + 8 * k;
   g->o_src = g->o_tw + 4 * k;
   g->o_row = g->o_src + 4;
-  g->disp_slot = align_up(g->o_row + 4, 16);
-  g->comb_slot = align_up(2 * (size_t)hidden + 4 * (size_t)k, 16);
+  g->o_can = g->o_row + 4;
+  g->disp_slot = align_up(g->o_can + 4, 16);
+  g->comb_can = 2 * (int64_t)hidden + 4 * (int64_t)k;
+  g->comb_slot = align_up(g->comb_can + 4, 16);
+  const char* nc = getenv("EPB_RING_UNSAFE_NO_CREDIT");
+  g->no_credit = nc != nullptr && nc[0] == '1';
   const int64_t per_token = R * lanes * (g->disp_slot + g->comb_slot);
   int64_t rt = (int64_t)c->cfg.nvl_bytes / per_token;
   int pow2 = 0;
