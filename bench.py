@@ -169,30 +169,50 @@ def cpu_baseline(world: int, budget_s: float = 12.0, threads: int = 1):
                       f"in {dt:.1f} s with the numpy oracle"}
 
 
+def _config_dict(world: int) -> dict:
+    """The workload description both arms print (identical dicts: same_config)."""
+    return {"workload": WORKLOAD, "ep": world, "tokens_per_rank": T_PER_RANK, "hidden": HIDDEN,
+            "experts": EXPERTS, "topk": TOPK, "parallelism": f"ep{world}"}
+
+
+def ref_sample_tokens(world: int) -> int:
+    """Tokens per simulated rank in one reference-arm step: the full 4096 at EP=1,
+    4096/EP^2 beyond, so a step's message count stays near the EP=1 one and the
+    whole --steps/--warmup run ends within a few minutes."""
+    return T_PER_RANK if world == 1 else max(32, T_PER_RANK // (world * world))
+
+
 def run_reference(args):
+    """The reference's own CPU implementation of the path (oracle/refpipe.py):
+    epsim's pack_fields -> SPSC ring (2 threads) -> unpack_fields + imm encode ->
+    apply_deliveries for the HT dispatch of every simulated rank, then the
+    oracle port's canonical combine (the reference has no combine code)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import ep as O
+    from oracle import refpipe
+    from tests.helpers import bf16_random, make_routing
     world = args.gpus
-    threads = max(1, len(os.sched_getaffinity(0)))
-    x, idx, w = _cpu_inputs(0, T_PER_RANK)
-    for _ in range(args.warmup):
-        _cpu_step(x, idx, w, world, threads)
-    t0 = time.perf_counter()
-    rows = 0
-    for _ in range(args.steps):
-        rows += _cpu_step(x, idx, w, world, threads)
-    dt = time.perf_counter() - t0
-    gbs = 2 * rows * ROW / dt / 1e9
+    Ts = ref_sample_tokens(world)
+    xs, in_ranks = [], []
+    for r in range(world):
+        g = np.random.default_rng(1000 + r)
+        idx, _ = make_routing(g, Ts, EXPERTS, TOPK)
+        xs.append(bf16_random(g, (Ts, HIDDEN)))
+        in_ranks.append(O.get_dispatch_layout(idx, EXPERTS, world)[2])
+    dt, step_bytes, backend, cores = refpipe.time_steps(xs, in_ranks, args.steps, args.warmup)
+    gbs = step_bytes / dt / 1e9
+    sample = (f"{world} simulated rank(s) x {Ts} tokens (of {T_PER_RANK}) per step; epsim ({backend}) pack_fields -> "
+              f"SPSC ring cap {refpipe.RING_CAP} -> unpack_fields + encode_ht_batch -> 50%-reordered "
+              f"apply_deliveries (HT, {refpipe.NCH} channels, 32-token chunks; single-threaded as shipped), then "
+              f"the numpy oracle's canonical combine on {cores} threads (the reference has no combine)")
     line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (seeded routing, N(0,1) bf16 tokens)",
-            "config": {"workload": WORKLOAD, "ep": world, "tokens_per_rank": T_PER_RANK, "hidden": HIDDEN,
-                       "experts": EXPERTS, "topk": TOPK, "parallelism": f"ep{world}"},
-            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-                             "sample": f"{args.steps} timed steps of rank 0's 4096-token workload (oracle numpy "
-                                       f"port of the reference path, {threads} threads)"},
+            "data": "synthetic (seeded routing, N(0,1) bf16 tokens)", "config": _config_dict(world),
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
+                             "sample": sample, "host_cores": len(os.sched_getaffinity(0))},
             "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -217,7 +237,7 @@ def run_ours(args):
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
 
     import paper_2512_19849_b200 as epb
-    from tests.helpers import bf16_random, make_routing
+    from tests import verify
 
     R = world
     dev = torch.device("cuda", local_rank)
@@ -226,15 +246,18 @@ def run_ours(args):
     buf = epb.Buffer(group, nvl, ll_bytes, low_latency_mode=True, fifo_channels=16, fifo_capacity=1024,
                      proxy_threads=4, ll_transport="nvlink")
 
-    # rotating input sets (4 x 58.7 MB > 126 MB L2)
+    # rotating input sets (4 x 58.7 MB > 126 MB L2); seeded so any rank can
+    # regenerate any other rank's set (oracle verification, tests/verify.py)
     NSETS = 4
     sets = []
+
+    def head_inputs(r, i=0):
+        idx, w = verify.routing(10_000 * r + i, T_PER_RANK, EXPERTS, TOPK)
+        return verify.seeded_x(torch, 10_000 * r + i, T_PER_RANK, HIDDEN, dev), idx, w
+
     for i in range(NSETS):
-        g = np.random.default_rng(10_000 * rank + i)
-        idx, w = make_routing(g, T_PER_RANK, EXPERTS, TOPK)
-        x = bf16_random(g, (T_PER_RANK, HIDDEN))
-        sets.append((torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev),
-                     torch.from_numpy(idx).to(dev), torch.from_numpy(w).to(dev)))
+        x, idx, w = head_inputs(rank, i)
+        sets.append((x, torch.from_numpy(idx).to(dev), torch.from_numpy(w).to(dev)))
     # payload rows this rank moves per step (dispatch rows = combine rows)
     rows, remote_rows = [], []
     for x, idx, w in sets:
@@ -273,6 +296,11 @@ def run_ours(args):
 
     for i in range(max(3, args.warmup)):
         step(i)
+    barrier()
+    # one step of set 0 checked against the oracle (untimed)
+    verified = {}
+    verified["headline"] = _verify(lambda: _verify_normal_step(buf, sets[0], lambda r: head_inputs(r, 0), rank, R,
+                                                               EXPERTS, None))
     barrier()
 
     # ---- timed region (device events) -----------------------------------------------
@@ -449,10 +477,11 @@ def run_ours(args):
                 "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded uniform top-8 routing, N(0,1) bf16 tokens)",
-                "config": {"workload": WORKLOAD, "ep": R, "tokens_per_rank": T_PER_RANK, "hidden": HIDDEN,
-                           "experts": EXPERTS, "topk": TOPK, "parallelism": f"ep{R}",
-                           "l2": f"{NSETS} rotating input sets ({NSETS * T_PER_RANK * ROW / 1e6:.0f} MB > 126 MB L2)"},
-                "per_gpu_gbs": round(value / R, 3),
+                "config": _config_dict(R),
+                "l2": f"{NSETS} rotating input sets ({NSETS * T_PER_RANK * ROW / 1e6:.0f} MB > 126 MB L2)",
+                "value_scope": "sum over all GPUs of the payload bytes each moves per step (dispatch + combine rows, "
+                               "local rows included) / max-over-ranks step time",
+                "per_gpu_gbs": round(value / R, 3), "verified": verified["headline"],
                 "kernels_ms": kernels_ms, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_scope": "per rank",
                 "clocks": clocks.summary(), "cpu_baseline": cpu}
@@ -461,6 +490,36 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _verify(fn):
+    """Run one oracle check (untimed); never let a failure take the bench line down."""
+    try:
+        info = fn()
+        return {"verified": True, **(info or {})}
+    except Exception as exc:  # noqa: BLE001
+        return {"verified": False, "verify_error": f"{type(exc).__name__}: {exc}"[:300]}
+
+
+def _verify_normal_step(buf, inp, inputs_fn, rank, R, E, fp8_cast, combine_copy=False):
+    """layout -> dispatch -> combine (identity experts) of one input set through the
+    public API, then tests/verify.py against the oracle on every rank."""
+    import torch
+    from tests import verify
+    x, idx, w = inp
+    x_in = fp8_cast(x) if fp8_cast else x
+    per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(idx, E)
+    recv_x, rti, rtw, lst, handle, _ = buf.dispatch(x_in, num_tokens_per_rank=per_rank, is_token_in_rank=in_rank,
+                                                    num_tokens_per_expert=per_exp, topk_idx=idx, topk_weights=w)
+    if fp8_cast:
+        y = recv_x[0].to(torch.bfloat16)
+    else:
+        y = recv_x.clone() if combine_copy else recv_x
+    out, out_w, _ = buf.combine(y, handle, topk_weights=rtw)
+    torch.cuda.synchronize()
+    buf._g.check_device_error()
+    return verify.verify_normal(torch, rank, R, E, inputs_fn, (recv_x, rti, rtw, lst, handle), (out, out_w),
+                                fp8_cast=fp8_cast, check_tokens=None if R == 1 else 512)
 
 
 def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T, H, E, fp8=False, zipf=0.0,
@@ -472,18 +531,26 @@ def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T,
     median over reps of the max over ranks, from CUDA events on the stream."""
     import torch
     import paper_2512_19849_b200 as epb
-    from tests.helpers import bf16_random, make_routing
     own = buf is None
     if own and ht == "ring":  # bounded rings: 74 lanes x 64 slots per peer, whatever T is (tools/ring_sweep.py)
         buf = epb.Buffer(group, epb.ring_nvl_bytes(H, R, TOPK, 74, 64), 0, ht_transport="ring", ring_lanes=74)
     elif own:
         buf = epb.Buffer(group, epb.nvl_bytes_hint(T, H, R, TOPK, 2, ht_proxy=ht == "proxy"), 0, num_recv_slots=2,
                          fifo_channels=8 if ht == "proxy" else 0, proxy_threads=4, ht_transport=ht)
-    g = np.random.default_rng(31_000 + 97 * rank + int(zipf * 10))
-    idx, w = make_routing(g, T, E, TOPK, zipf=zipf)
-    x = torch.from_numpy(bf16_random(g, (T, H)).view(np.int16)).view(torch.bfloat16).to(dev)
+    from tests import verify
+
+    def inputs(r):
+        seed = 31_000 + 97 * r + int(zipf * 10)
+        idx, w = verify.routing(seed, T, E, TOPK, zipf=zipf)
+        return verify.seeded_x(torch, seed, T, H, dev), idx, w
+
+    x, idx, w = inputs(rank)
     idx_t, w_t = torch.from_numpy(idx).to(dev), torch.from_numpy(w).to(dev)
     x_in = epb.per_token_cast_to_fp8(x) if fp8 else x
+    check = _verify(lambda: _verify_normal_step(buf, (x, idx_t, w_t), inputs, rank, R, E,
+                                                epb.per_token_cast_to_fp8 if fp8 else None,
+                                                combine_copy=not combine_in_region))
+    barrier()
     row_bytes = (H + 4 * (H // 128)) if fp8 else 2 * H
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     m = torch.zeros(T, R, dtype=torch.bool, device=dev)
@@ -493,8 +560,10 @@ def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T,
     reps = max(10, min(args.steps, 30))
     d_ms, c_ms = [], []
     try:
-        return _config_loop(buf, own, idx_t, w_t, x_in, fp8, combine_in_region, flush, remote, reps, T, H, E, zipf, ht,
-                            row_bytes, R, dev, barrier, max_over_ranks, d_ms, c_ms)
+        out = _config_loop(buf, own, idx_t, w_t, x_in, fp8, combine_in_region, flush, remote, reps, T, H, E, zipf, ht,
+                           row_bytes, R, dev, barrier, max_over_ranks, d_ms, c_ms)
+        out.update(check)
+        return out
     except Exception:
         if ht == "proxy":
             _proxy_diag(buf, rank)
@@ -598,20 +667,25 @@ def y_in_region(fp8, combine_in_region):
 
 def ll_bench(buf, transport, rank, R, dev, args, barrier, max_over_ranks):
     import torch
-    from tests.helpers import bf16_random, make_routing
-    import paper_2512_19849_b200 as epb
     from paper_2512_19849_b200._lib import check, lib
     if transport == "proxy" and not buf._rank.proxy_running:
         check(lib.epb_proxy_start(buf._rank.ctx))
         buf._rank.proxy_running = True
     buf.ll_transport = transport
-    g = np.random.default_rng(77 + rank)
-    idx, w = make_routing(g, LL_TOKENS, EXPERTS, TOPK)
-    x = torch.from_numpy(bf16_random(g, (LL_TOKENS, HIDDEN)).view(np.int16)).view(torch.bfloat16).to(dev)
+    from tests import verify
+    L = EXPERTS // R
+
+    def inputs(r):
+        idx, w = verify.routing(77 + r, LL_TOKENS, EXPERTS, TOPK)
+        return verify.seeded_x(torch, 77 + r, LL_TOKENS, HIDDEN, dev), idx, w
+
+    def ys(r):  # rank r's expert outputs (seeded: every rank can regenerate them)
+        return verify.seeded_x(torch, 88 + r, L * R * LL_TOKENS, HIDDEN, dev).view(L, R * LL_TOKENS, HIDDEN)
+
+    x, idx, w = inputs(rank)
     idx_t = torch.from_numpy(idx).to(dev)
     w_t = torch.from_numpy(w).to(dev)
-    L = EXPERTS // R
-    y = torch.randn(L, R * LL_TOKENS, HIDDEN, device=dev).to(torch.bfloat16)
+    y = ys(rank)
 
     def once():
         recv, count, handle, _, _ = buf.low_latency_dispatch(x, idx_t, LL_TOKENS, EXPERTS, use_fp8=True)
@@ -638,6 +712,15 @@ def ll_bench(buf, transport, rank, R, dev, args, barrier, max_over_ranks):
 
     eager_us = timed(once, n)
     out = {"tokens": LL_TOKENS, "fp8": True, "eager_step_us": round(eager_us, 2)}
+
+    def check():
+        recv, count, handle, _, _ = buf.low_latency_dispatch(x, idx_t, LL_TOKENS, EXPERTS, use_fp8=True)
+        comb, _, _ = buf.low_latency_combine(y, idx_t, w_t, handle)
+        torch.cuda.synchronize()
+        buf._g.check_device_error()
+        return verify.verify_ll(torch, rank, R, EXPERTS, LL_TOKENS, inputs, ys, recv, count, handle, comb)
+    out.update(_verify(check))
+    barrier()
     # decode runs dispatch+combine inside CUDA graphs (epochs are device-resident,
     # so a captured pair replays correctly); replayed back to back this is the
     # device latency of the pair, free of Python launch overhead

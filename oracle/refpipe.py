@@ -195,6 +195,10 @@ class HTDispatchStep:
             self.regions[s, : self.T * self.row] = xs[s].view(np.uint8).reshape(-1)
         self.n_ctr = 2 * self.R * NCH
         self.rows = int(sum(ir.sum() for ir in in_ranks))
+        from concurrent.futures import ThreadPoolExecutor
+        self.threads = max(1, len(os.sched_getaffinity(0)))
+        self.pool = ThreadPoolExecutor(self.threads)
+        self.tok_chunk = max(1, -(-self.T // self.threads))
 
     def run(self):
         """One timed step: returns the combined outputs (per source) after checking the delivery."""
@@ -235,6 +239,8 @@ class HTDispatchStep:
         return np.concatenate(parts, axis=0)
 
     def _combine(self):
+        """The oracle port's canonical combine, token ranges spread over every host
+        core (numpy releases the GIL in the gathers and adds)."""
         from oracle import ep as O
         recv = [self._recv(d) for d in range(self.R)]
         heads = []
@@ -243,11 +249,19 @@ class HTDispatchStep:
             heads.append(np.where(ir, np.cumsum(ir, axis=0) - 1, -1).astype(np.int32))
         counts = np.array([[int(self.in_ranks[s][:, d].sum()) for d in range(self.R)] for s in range(self.R)])
         rpm = np.cumsum(counts, axis=0).astype(np.int32)
-        return recv, O.combine(recv, self.in_ranks, heads, rpm)
+        jobs = [(s, a, min(a + self.tok_chunk, self.T)) for s in range(self.R) for a in range(0, self.T, self.tok_chunk)]
+        parts = list(self.pool.map(
+            lambda j: O.combine_rank(j[0], recv, self.in_ranks[j[0]][j[1]:j[2]], heads[j[0]][j[1]:j[2]], rpm)[0], jobs))
+        out, i = [], 0
+        for s in range(self.R):
+            n = -(-self.T // self.tok_chunk)
+            out.append(np.concatenate(parts[i:i + n], axis=0))
+            i += n
+        return recv, out
 
 
 def time_steps(xs, in_ranks, steps: int, warmup: int, seed: int = 0):
-    """(seconds per step, payload bytes per step [dispatch + combine rows], backend)."""
+    """(seconds per step, payload bytes per step [dispatch + combine rows], backend, host threads)."""
     st = HTDispatchStep(xs, in_ranks, seed)
     for _ in range(max(1, warmup)):
         st.run()
@@ -255,4 +269,5 @@ def time_steps(xs, in_ranks, steps: int, warmup: int, seed: int = 0):
     for _ in range(steps):
         st.run()
     dt = (time.perf_counter() - t0) / max(1, steps)
-    return dt, 2 * st.rows * st.row, st.ep.backend
+    st.pool.shutdown()
+    return dt, 2 * st.rows * st.row, st.ep.backend, st.threads

@@ -26,7 +26,10 @@ def make_routing(g: np.random.Generator, T: int, E: int, k: int, mask_frac: floa
         perm = g.permutation(E)
         pop = np.empty(E)
         pop[perm] = p / p.sum()
-        idx = np.stack([g.choice(E, size=k, replace=False, p=pop) for _ in range(T)]) if T else np.zeros((0, k), int)
+        # k draws without replacement with probability ~ pop: the top-k of
+        # log(pop) + Gumbel noise (the Gumbel-top-k trick), vectorised over tokens
+        key = np.log(pop)[None, :] - np.log(-np.log(g.random((T, E))))
+        idx = np.argsort(-key, axis=1)[:, :k] if T else np.zeros((0, k), int)
     else:
         idx = np.argsort(g.random((T, E)), axis=1)[:, :k] if T else np.zeros((0, k), int)
     idx = idx.astype(np.int64)
