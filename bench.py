@@ -42,6 +42,7 @@ import numpy as np  # noqa: E402
 
 T_PER_RANK, HIDDEN, EXPERTS, TOPK = 4096, 7168, 256, 8
 LL_TOKENS = 128
+NSLOTS = 6  # receive slots: one per captured step graph (4 rotating sets) + eager + the scratch slot
 ROW = HIDDEN * 2
 WORKLOAD = "DeepSeek-V3 normal mode: 4096 tok/rank, hidden 7168, 256 experts, top-8, bf16 dispatch + bf16 combine"
 METRIC = "dispatch/combine GB/s per GPU at 1/2/4/8 B200 (+ LL µs) vs NVLink roofline"
@@ -241,10 +242,10 @@ def run_ours(args):
 
     R = world
     dev = torch.device("cuda", local_rank)
-    nvl = epb.nvl_bytes_hint(T_PER_RANK, HIDDEN, R, TOPK, 3)
+    nvl = epb.nvl_bytes_hint(T_PER_RANK, HIDDEN, R, TOPK, NSLOTS)
     ll_bytes = epb.Buffer.get_low_latency_rdma_size_hint(LL_TOKENS, HIDDEN, R, EXPERTS, num_topk=TOPK)
-    buf = epb.Buffer(group, nvl, ll_bytes, low_latency_mode=True, fifo_channels=16, fifo_capacity=1024,
-                     proxy_threads=4, ll_transport="nvlink")
+    buf = epb.Buffer(group, nvl, ll_bytes, low_latency_mode=True, num_recv_slots=NSLOTS, fifo_channels=16,
+                     fifo_capacity=1024, proxy_threads=4, ll_transport="nvlink")
 
     # rotating input sets (4 x 58.7 MB > 126 MB L2); seeded so any rank can
     # regenerate any other rank's set (oracle verification, tests/verify.py)
@@ -303,37 +304,70 @@ def run_ours(args):
                                                                EXPERTS, None))
     barrier()
 
-    # ---- timed region (device events) -----------------------------------------------
+    # ---- CUDA-graph steps -----------------------------------------------------------
+    # num_worst_tokens = R*T (DeepEP's worst-case sizing): the dispatch needs no
+    # host sync, so layout -> dispatch -> combine of one input set is captured
+    # as one graph; one graph per rotating set (its inputs are the set's static
+    # tensors).  Replays are the serving loop: every replay does the step's full
+    # work (the kernels move only the real rows).
+    n_worst = R * T_PER_RANK
+    cap_stream = torch.cuda.Stream(device=dev)
+
+    def graph_step(i, ev=None):
+        x, idx, w = sets[i % NSETS]
+        if ev:
+            ev[0].record()
+        per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(idx, EXPERTS)
+        if ev:
+            ev[1].record()
+        recv_x, rti, rtw, _, handle, _ = buf.dispatch(x, num_tokens_per_rank=per_rank, is_token_in_rank=in_rank,
+                                                      num_tokens_per_expert=per_exp, topk_idx=idx, topk_weights=w,
+                                                      num_worst_tokens=n_worst)
+        if ev:
+            ev[2].record()
+        out, out_w, _ = buf.combine(recv_x, handle, topk_weights=rtw)
+        if ev:
+            ev[3].record()
+        return out, (per_rank, per_exp, in_rank, recv_x, rti, rtw, handle, out_w)
+
+    def capture(with_events: bool):
+        graphs = []
+        cap_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cap_stream):
+            for i in range(NSETS):  # warm-up on the capture stream (every rank runs it)
+                graph_step(i)
+            cap_stream.synchronize()
+            if world > 1:
+                dist.barrier()
+            for i in range(NSETS):
+                g = torch.cuda.CUDAGraph()
+                ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)] if with_events else None
+                with torch.cuda.graph(g, stream=cap_stream):
+                    out, keep = graph_step(i, ev)
+                graphs.append((g, out, keep, ev))
+        torch.cuda.current_stream().wait_stream(cap_stream)
+        barrier()
+        return graphs
+
+    graphs = capture(False)
+    for i in range(max(3, args.warmup)):
+        graphs[i % NSETS][0].replay()
+    barrier()
+    verified["graph"] = _verify(lambda: _verify_graph_step(graphs[0], sets[0], lambda r: head_inputs(r, 0), rank, R,
+                                                           EXPERTS))
+    barrier()
+
+    # ---- timed region (device events around K graph replays) ------------------------------
     clocks = Clocks(local_rank)
     with clocks:
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         for i in range(args.steps):
-            step(i)
+            graphs[i % NSETS][0].replay()
         ev1.record()
         barrier()
     ms_local = ev0.elapsed_time(ev1)
-    # per-launch device times from a second, profiled pass of the same steps.
-    # A short device spin is queued ahead of every op so its start event and
-    # launch are already in the stream when the GPU reaches them: the events
-    # bracket the kernel alone, not the host's launch latency.
-    spin_cycles = int(30e-6 * _sm_hz(local_rank))
-    prof = []
-    with epb.buffer.profiling(prof):
-        for i in range(args.steps):
-            x, idx, w = sets[i % NSETS]
-            torch.cuda._sleep(spin_cycles)
-            per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(idx, EXPERTS)
-            torch.cuda._sleep(spin_cycles)
-            recv_x, rti, rtw, _, handle, _ = buf.dispatch(x, num_tokens_per_rank=per_rank, is_token_in_rank=in_rank,
-                                                          num_tokens_per_expert=per_exp, topk_idx=idx, topk_weights=w)
-            torch.cuda._sleep(spin_cycles)
-            buf.combine(recv_x, handle, topk_weights=rtw)
-        barrier()
-    per_kernel = {}
-    for name, ms_k in prof:
-        per_kernel.setdefault(name, []).append(ms_k)
     ms = max_over_ranks(ms_local)
     my_rows = sum(rows[i % NSETS] for i in range(args.steps))
     my_remote = sum(remote_rows[i % NSETS] for i in range(args.steps))
@@ -341,6 +375,38 @@ def run_ours(args):
     value = job_bytes / (ms / 1e3) / 1e9
     ms_per_step = ms / args.steps
     launches_per_step = 3  # layout, dispatch (count exchange fused), combine
+
+    # the same steps eager (host-launched, counts read back by the host every step)
+    for i in range(3):
+        step(i)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        step(i)
+    e1.record()
+    barrier()
+    ms_eager = max_over_ranks(e0.elapsed_time(e1))
+    eager = {"value": round(job_bytes / (ms_eager / 1e3) / 1e9, 3), "ms_per_step": round(ms_eager / args.steps, 4),
+             "mode": "eager host launches; the host waits for the receive counts each dispatch"}
+    del graphs
+    barrier()
+
+    # per-kernel device times: graphs with external event nodes between the ops
+    pgraphs = capture(True)
+    for i in range(NSETS):
+        pgraphs[i][0].replay()
+    barrier()
+    per_kernel = {"layout": [], "dispatch": [], "combine": []}
+    for i in range(args.steps):
+        g, _, _, ev = pgraphs[i % NSETS]
+        g.replay()
+        torch.cuda.synchronize()
+        per_kernel["layout"].append(ev[0].elapsed_time(ev[1]))
+        per_kernel["dispatch"].append(ev[1].elapsed_time(ev[2]))
+        per_kernel["combine"].append(ev[2].elapsed_time(ev[3]))
+    del pgraphs
+    barrier()
 
     # ---- roofline of the dominant kernel -------------------------------------------------
     hbm_peak, peak_kind = _peaks()
@@ -365,36 +431,37 @@ def run_ours(args):
     roofline = {"bound": bound, "kernel": dom, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind if R == 1 else
                 "B200_PROFILING.md measured peer copy (770 GB/s/direction)",
-                "algorithmic_bytes_per_launch": int(algo), "avg_launch_ms": round(avg[dom], 4)}
+                "algorithmic_bytes_per_launch": int(algo), "avg_launch_ms": round(avg[dom], 4),
+                "timing": "CUDA events (external graph nodes) around the kernel inside the replayed step graph"}
     kernels_ms = {k: round(v, 4) for k, v in avg.items()}
 
     # ---- end to end from pinned host buffers ---------------------------------------------
-    hx = [s[0].cpu().pin_memory() for s in sets]
-    hidx = [s[1].cpu().pin_memory() for s in sets]
-    hw = [s[2].cpu().pin_memory() for s in sets]
+    # Pipelined like a serving loop: step i+1's inputs go up on an H2D stream
+    # into the static inputs of the graph that runs it, step i-1's result comes
+    # down on a D2H stream while step i's graph replays (PCIe is full duplex).
+    # Every step still moves its own inputs and result.
+    egraphs = capture(False)
+    hx = [s_[0].cpu().pin_memory() for s_ in sets]
+    hidx = [s_[1].cpu().pin_memory() for s_ in sets]
+    hw = [s_[2].cpu().pin_memory() for s_ in sets]
     hout = [torch.empty((T_PER_RANK, HIDDEN), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-    # Pipelined like a serving loop: step i+1's inputs go up on an H2D stream and
-    # step i-1's result comes down on a D2H stream while step i computes (PCIe
-    # is full duplex).  Every step still moves its own inputs and result.
-    dx = [torch.empty_like(sets[0][0]) for _ in range(2)]
-    didx = [torch.empty_like(sets[0][1]) for _ in range(2)]
-    dw = [torch.empty_like(sets[0][2]) for _ in range(2)]
     comp = torch.cuda.current_stream()
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
 
     def e2e_run(n):
-        done = [None, None]  # compute event of the last step that used device input buffer b
-        outev = [None, None]  # D2H event of the last copy into host buffer b
+        done = [None] * NSETS  # compute event of the last replay of graph j (its inputs are free after it)
+        outev = [None, None]   # D2H event of the last copy into host buffer b
+        outsrc = [None] * NSETS  # D2H event of the last copy out of graph j's output
         up = []
 
         def upload(i):
-            b, j = i % 2, i % NSETS
+            j = i % NSETS
             with torch.cuda.stream(s_h2d):
-                if done[b] is not None:
-                    s_h2d.wait_event(done[b])
-                dx[b].copy_(hx[j], non_blocking=True)
-                didx[b].copy_(hidx[j], non_blocking=True)
-                dw[b].copy_(hw[j], non_blocking=True)
+                if done[j] is not None:
+                    s_h2d.wait_event(done[j])
+                sets[j][0].copy_(hx[j], non_blocking=True)
+                sets[j][1].copy_(hidx[j], non_blocking=True)
+                sets[j][2].copy_(hw[j], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(s_h2d)
             up.append(ev)
@@ -406,25 +473,23 @@ def run_ours(args):
         for i in range(n):
             if i + 1 < n:
                 upload(i + 1)
-            b = i % 2
+            j, b = i % NSETS, i % 2
             comp.wait_event(up[i])
-            per_rank, _, per_exp, in_rank, _ = buf.get_dispatch_layout(didx[b], EXPERTS)
-            recv_x, rti, rtw, _, handle, _ = buf.dispatch(dx[b], num_tokens_per_rank=per_rank,
-                                                          is_token_in_rank=in_rank, num_tokens_per_expert=per_exp,
-                                                          topk_idx=didx[b], topk_weights=dw[b])
-            out, _, _ = buf.combine(recv_x, handle, topk_weights=rtw)
+            if outsrc[j] is not None:
+                comp.wait_event(outsrc[j])  # the graph's output buffer was read out
+            egraphs[j][0].replay()
             ev = torch.cuda.Event()
             ev.record(comp)
-            done[b] = ev
+            done[j] = ev
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev)
                 if outev[b] is not None:
                     s_d2h.wait_event(outev[b])
-                hout[b].copy_(out, non_blocking=True)
-                out.record_stream(s_d2h)
+                hout[b].copy_(egraphs[j][1], non_blocking=True)
                 oe = torch.cuda.Event()
                 oe.record(s_d2h)
                 outev[b] = oe
+                outsrc[j] = oe
         for b in range(2):
             if outev[b] is not None:
                 comp.wait_event(outev[b])
@@ -441,7 +506,9 @@ def run_ours(args):
     d2h = T_PER_RANK * ROW
     e2e = {"value": round(job_bytes / (e2e_ms / 1e3) / 1e9, 4), "unit": "GB/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms / args.steps, 4),
-           "pipelining": "H2D of step i+1 and D2H of step i-1 overlap step i (separate copy streams)"}
+           "pipelining": "H2D of step i+1 and D2H of step i-1 overlap step i's graph replay (separate copy streams)"}
+    del egraphs
+    barrier()
 
     # ---- the other normal-mode rows of BASELINE.json (per-op device times) -------------------
     configs = {}
@@ -481,8 +548,11 @@ def run_ours(args):
                 "l2": f"{NSETS} rotating input sets ({NSETS * T_PER_RANK * ROW / 1e6:.0f} MB > 126 MB L2)",
                 "value_scope": "sum over all GPUs of the payload bytes each moves per step (dispatch + combine rows, "
                                "local rows included) / max-over-ranks step time",
-                "per_gpu_gbs": round(value / R, 3), "verified": verified["headline"],
-                "kernels_ms": kernels_ms, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
+                "per_gpu_gbs": round(value / R, 3),
+                "verified": {"verified": all(v.get("verified") for v in verified.values()), **verified},
+                "step_mode": f"CUDA graph per step (layout -> dispatch(num_worst_tokens={n_worst}) -> combine), "
+                             "replayed back to back",
+                "eager": eager, "kernels_ms": kernels_ms, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_scope": "per rank",
                 "clocks": clocks.summary(), "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
@@ -520,6 +590,21 @@ def _verify_normal_step(buf, inp, inputs_fn, rank, R, E, fp8_cast, combine_copy=
     buf._g.check_device_error()
     return verify.verify_normal(torch, rank, R, E, inputs_fn, (recv_x, rti, rtw, lst, handle), (out, out_w),
                                 fp8_cast=fp8_cast, check_tokens=None if R == 1 else 512)
+
+
+def _verify_graph_step(graph, inp, inputs_fn, rank, R, E):
+    """One replay of a captured step graph (num_worst_tokens outputs) against the oracle."""
+    import torch
+    from tests import verify
+    g, out, keep, _ = graph
+    g.replay()
+    torch.cuda.synchronize()
+    per_rank, per_exp, in_rank, recv_x, rti, rtw, handle, out_w = keep
+    n = int(handle[0][R - 1, rank])  # real receive rows (rank_prefix_matrix)
+    assert (rti[n:] == -1).all(), "rows past the real count must carry no expert"
+    h = tuple(t[:n] if i == 3 else t for i, t in enumerate(handle))
+    return verify.verify_normal(torch, rank, R, E, inputs_fn, (recv_x[:n], rti[:n], rtw[:n], [], h), (out, out_w),
+                                check_tokens=None if R == 1 else 512, check_per_expert=False)
 
 
 def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T, H, E, fp8=False, zipf=0.0,

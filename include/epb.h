@@ -96,6 +96,8 @@ int epb_trace(epb_t* ctx, int64_t* out64);
 int epb_debug_stamp(int64_t* dst, void* stream);
 /* Diagnostics: byte offset of the proxy HT signal counters in a region. */
 int64_t epb_debug_ht_sig_offset(void);
+/* Byte offset of the arena inside a region (TransferCmd offsets are relative to it). */
+int64_t epb_arena_offset(void);
 /* Base device address of this rank's symmetric region and its size. */
 int epb_region(epb_t* ctx, void** base, size_t* bytes);
 
@@ -139,6 +141,11 @@ typedef struct {
   int32_t* channel_prefix_matrix;      /* [R, C]  my sends, inclusive over chan */
   int32_t* recv_channel_prefix_matrix; /* [R, C]  my receives, inclusive        */
   int32_t* send_head;                  /* [T, R]  row of t inside my block at r, -1 */
+  /* DeepEP num_worst_tokens: > 0 = the caller sized its receive views for this
+     many rows and does not wait for the counts (no host sync, CUDA-graph
+     capturable); rows [N_recv, num_worst_tokens) get recv_topk_idx = -1 and a
+     call receiving more rows aborts with EPB_ERR_CONFIG */
+  int num_worst_tokens;
 } epb_dispatch_args_t;
 
 /* One cooperative launch: per-channel counts, the cross-rank count exchange
@@ -371,6 +378,30 @@ int epb_barrier_open(const char* name, int world, int rank, epb_barrier_t** out)
 int epb_barrier_wait(epb_barrier_t* b, int same_rail, double timeout_s);
 int epb_barrier_close(epb_barrier_t* b, int unlink_segment);
 int epb_proxy_barrier(epb_t* ctx, int channel, int same_rail, void* stream);
+
+/* Drain(Idx): a kernel pushes a DRAIN command
+ * on `channel` (length_or_value = upto + 1; upto < 0: everything issued so far)
+ * and spins on check_completion of it; the proxy completes it once every copy
+ * issued for commands <= upto of that channel has landed.  Blocking on the GPU
+ * side, stream-ordered. */
+int epb_proxy_drain(epb_t* ctx, int channel, int64_t upto, void* stream);
+/* Test producer for Drain(Idx): a kernel pushes n WRITEs (block i of `bytes`
+ * from src_off + i*bytes to dst_off + i*bytes at rank dst, arena offsets) then
+ * Drain(upto-th of them); after it completes, result[i] (device int32 [n+1]) =
+ * 1 if block i had landed, result[n] = ns from the drain push to completion. */
+int epb_debug_drain_test(epb_t* ctx, int channel, int dst, int n, int64_t src_off, int64_t dst_off, int64_t bytes,
+                         int64_t upto, int32_t* result, void* stream);
+
+/* Phase trace of a STOPPED proxy (EPB_TRACE=1): rows of 4 int64 {host
+ * CLOCK_REALTIME ns, kind, a, b}; kind 1 = tail seen (a = channel, b = tail),
+ * 2 = copy issued (a = dst, b = bytes), 3 = value write issued (a = dst,
+ * b = value), 4 = COMPLETED published (a = channel, b = value).  Returns the
+ * number of events (copies min(n, max_events) into out). */
+int64_t epb_proxy_trace(epb_t* ctx, int64_t* out, int64_t max_events);
+
+/* %globaltimer - CLOCK_REALTIME offset (ns) and its uncertainty, for lining up
+ * kernel phase marks with the proxy's host events. */
+int epb_clock_calibrate(int64_t* offset_ns, int64_t* error_ns);
 
 #ifdef __cplusplus
 }

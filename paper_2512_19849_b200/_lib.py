@@ -58,7 +58,8 @@ class DispatchArgs(C.Structure):
                 ("topk_idx", vp), ("topk_weights", vp), ("num_topk", C.c_int), ("is_token_in_rank", vp),
                 ("num_tokens_per_expert", vp), ("num_tokens", C.c_int), ("num_experts", C.c_int),
                 ("expert_alignment", C.c_int), ("recv_slot", C.c_int), ("rank_prefix_matrix", vp),
-                ("channel_prefix_matrix", vp), ("recv_channel_prefix_matrix", vp), ("send_head", vp)]
+                ("channel_prefix_matrix", vp), ("recv_channel_prefix_matrix", vp), ("send_head", vp),
+                ("num_worst_tokens", C.c_int)]
 
 
 class CombineArgs(C.Structure):
@@ -170,6 +171,11 @@ _proto("epb_barrier_open", c_int, C.c_char_p, c_int, c_int, C.POINTER(vp))
 _proto("epb_barrier_wait", c_int, vp, c_int, c_double)
 _proto("epb_barrier_close", c_int, vp, c_int)
 _proto("epb_proxy_barrier", c_int, vp, c_int, c_int, vp)
+_proto("epb_proxy_drain", c_int, vp, c_int, i64, vp)
+_proto("epb_arena_offset", i64)
+_proto("epb_debug_drain_test", c_int, vp, c_int, c_int, c_int, i64, i64, i64, i64, vp, vp)
+_proto("epb_proxy_trace", i64, vp, P64, i64)
+_proto("epb_clock_calibrate", c_int, P64, P64)
 
 # every symbol include/epb.h declares (checked by tests/test_abi.py)
 EXPORTED = [
@@ -182,7 +188,8 @@ EXPORTED = [
     "epb_ring_pop_batch", "epb_ring_poll", "epb_ring_mark_completed", "epb_ring_check_completion",
     "epb_ring_shutdown", "epb_apply_deliveries", "epb_fifo_ctl", "epb_proxy_start", "epb_proxy_stop",
     "epb_proxy_stats", "epb_fifo_device_bench", "epb_barrier_open", "epb_barrier_wait", "epb_barrier_close",
-    "epb_proxy_barrier",
+    "epb_proxy_barrier", "epb_proxy_drain", "epb_debug_drain_test", "epb_proxy_trace", "epb_clock_calibrate",
+    "epb_arena_offset",
 ]
 
 

@@ -203,7 +203,7 @@ class _Group:
         return out
 
     def dispatch(self, xs, handles, is_token_in_ranks, num_tokens_per_experts, topk_idxs, topk_weights_list,
-                 expert_alignment: int, config: Optional[Config]):
+                 expert_alignment: int, config: Optional[Config], num_worst_tokens: int = 0):
         n = len(self.ranks)
         cfg = config or Config()
         # one block per channel; all blocks of all local ranks must be co-resident
@@ -221,12 +221,13 @@ class _Group:
             in_ranks = [h[4] for h in handles]
             none = [None] * n
             return X.dispatch(self.native, list(xd), list(xsc), in_ranks, none, none, none, expert_alignment,
-                              channels, self.timeout_s)
+                              channels, self.timeout_s, int(num_worst_tokens))
         for ir in is_token_in_ranks:
             if ir is None:
                 raise ConfigError("is_token_in_rank is required without a handle")
         return X.dispatch(self.native, list(xd), list(xsc), list(is_token_in_ranks), list(num_tokens_per_experts),
-                          list(topk_idxs), list(topk_weights_list), expert_alignment, channels, self.timeout_s)
+                          list(topk_idxs), list(topk_weights_list), expert_alignment, channels, self.timeout_s,
+                          int(num_worst_tokens))
 
     def combine(self, xs, handles, topk_weights_list, config: Optional[Config]):
         cfg = config or Config()
@@ -270,6 +271,74 @@ def _wait(previous_event: Optional[EventOverlap]) -> None:
         previous_event.current_stream_wait()
 
 
+def _tensors(obj, out=None):
+    out = [] if out is None else out
+    if isinstance(obj, torch.Tensor):
+        out.append(obj)
+    elif isinstance(obj, (tuple, list)):
+        for o in obj:
+            _tensors(o, out)
+    return out
+
+
+def _record(t: torch.Tensor, stream) -> None:
+    try:  # zero-copy views of the symmetric region are not caching-allocator memory
+        t.record_stream(stream)
+    except RuntimeError:
+        pass
+
+
+class _CommStream:
+    """DeepEP's stream discipline for one op (deep_ep Buffer: previous_event /
+    async_finish / allocate_on_comm_stream).  The op runs on the Buffer's comm
+    stream after ``previous_event`` (or after the current compute stream); with
+    async_finish the caller gets an EventOverlap on the comm stream and the
+    tensors involved are recorded on it, otherwise the compute stream waits
+    for the comm stream before the call returns.  With none of the three
+    options the op runs on the compute stream directly (the same ordering,
+    without the stream hops)."""
+
+    def __init__(self, buf: "Buffer", previous_event, async_finish: bool, allocate_on_comm_stream: bool, inputs=()):
+        self.active = previous_event is not None or async_finish or allocate_on_comm_stream
+        self.buf, self.prev, self.async_finish, self.inputs = buf, previous_event, async_finish, inputs
+
+    def __enter__(self):
+        if not self.active:
+            return self
+        self.compute = torch.cuda.current_stream()
+        comm = self.buf._comm_stream()
+        if self.prev is not None and self.prev.event is not None:
+            comm.wait_event(self.prev.event)
+        else:
+            comm.wait_stream(self.compute)
+        self.ctx = torch.cuda.stream(comm)
+        self.ctx.__enter__()
+        return self
+
+    def finish(self, result) -> EventOverlap:
+        if not self.active:
+            return EventOverlap(None)
+        self.ctx.__exit__(None, None, None)
+        comm = self.buf._comm_stream()
+        ts = _tensors(result) + _tensors(self.inputs)
+        if self.async_finish:
+            ev = torch.cuda.Event()
+            ev.record(comm)
+            for t in ts:  # caching-allocator safety: in use on both streams
+                _record(t, comm)
+                _record(t, self.compute)
+            return EventOverlap(ev, ts)
+        self.compute.wait_stream(comm)
+        for t in _tensors(result):
+            _record(t, self.compute)
+        return EventOverlap(None)
+
+    def __exit__(self, exc_type, exc, tb):
+        if exc_type is not None and self.active:
+            self.ctx.__exit__(exc_type, exc, tb)
+        return False
+
+
 class Buffer:
     """DeepEP-compatible communication buffer for one EP rank (one process per GPU)."""
 
@@ -311,6 +380,8 @@ class Buffer:
         self._g = _Group([self._rank], ht_transport, ring_lanes)
         self._native = self._rank.native
         self._sms_key, self._sms_val = None, 0
+        self._comm = None
+        self._ll_comb_bufs = {}
         self._destroyed = False
 
     def start_proxy(self) -> None:
@@ -354,8 +425,15 @@ class Buffer:
         t = mem[offset:].view(dtype)
         return t if size is None else t[: int(torch.Size(size).numel())].view(size)
 
+    def _comm_stream(self) -> torch.cuda.Stream:
+        if self._comm is None:
+            self._comm = torch.cuda.Stream(device=self._rank.device)
+        return self._comm
+
     def get_comm_stream(self) -> torch.cuda.Stream:
-        return torch.cuda.current_stream()
+        """The stream ops run on when async_finish / previous_event /
+        allocate_on_comm_stream are given (DeepEP Buffer.get_comm_stream)."""
+        return self._comm_stream()
 
     def destroy(self) -> None:
         if not self._destroyed:
@@ -385,9 +463,10 @@ class Buffer:
     def get_dispatch_layout(self, topk_idx: torch.Tensor, num_experts: int,
                             previous_event: Optional[EventOverlap] = None, async_finish: bool = False,
                             allocate_on_comm_stream: bool = False):
-        _wait(previous_event)
-        per_rank, per_expert, in_rank = X.layout(topk_idx, num_experts, self.group_size)
-        return per_rank, None, per_expert, in_rank, _event(async_finish)
+        with _CommStream(self, previous_event, async_finish, allocate_on_comm_stream, (topk_idx,)) as cs:
+            per_rank, per_expert, in_rank = X.layout(topk_idx, num_experts, self.group_size)
+            ev = cs.finish((per_rank, per_expert, in_rank))
+        return per_rank, None, per_expert, in_rank, ev
 
     # -- normal mode --------------------------------------------------------------
     def dispatch(self, x: Union[torch.Tensor, Tuple[torch.Tensor, torch.Tensor]], handle: Optional[tuple] = None,
@@ -399,8 +478,15 @@ class Buffer:
                  num_worst_tokens: int = 0, config: Optional[Config] = None,
                  previous_event: Optional[EventOverlap] = None, async_finish: bool = False,
                  allocate_on_comm_stream: bool = False):
-        if previous_event is not None:
-            previous_event.current_stream_wait()
+        with _CommStream(self, previous_event, async_finish, allocate_on_comm_stream,
+                         (x, topk_idx, topk_weights, is_token_in_rank)) as cs:
+            r = self._dispatch(x, handle, is_token_in_rank, num_tokens_per_expert, topk_idx, topk_weights,
+                               expert_alignment, num_worst_tokens, config)
+            ev = cs.finish((r[0], r[1], r[2], r[4]))
+        return r[0], r[1], r[2], r[3], r[4], ev
+
+    def _dispatch(self, x, handle, is_token_in_rank, num_tokens_per_expert, topk_idx, topk_weights, expert_alignment,
+                  num_worst_tokens, config):
         xd, xs = (x[0], x[1]) if isinstance(x, tuple) else (x, None)
         if self.ht_transport == "ring":
             if handle is None and is_token_in_rank is None:
@@ -408,30 +494,33 @@ class Buffer:
             (r,) = self._g.dispatch([x], [handle], [is_token_in_rank], [num_tokens_per_expert], [topk_idx],
                                     [topk_weights], expert_alignment, self._config(config))
             if handle is not None:
-                return r[0], None, None, None, None, _event(async_finish)
-            return r[0], r[1], r[2], r[3], r[4], _event(async_finish)
+                return r[0], None, None, None, None
+            return r[0], r[1], r[2], r[3], r[4]
+        if num_worst_tokens and self.ht_transport != "nvlink":
+            raise UnsupportedOperation("num_worst_tokens needs ht_transport='nvlink' (the proxy and ring transports "
+                                       "size their outputs from a host sync)")
         if handle is not None:  # cached layout: the handle carries is_token_in_rank
             r = X.dispatch1(self._native, xd, xs, handle[4], None, None, None, expert_alignment, self._sms(config),
-                            self._g.timeout_s)
-            return r[0], None, None, None, None, _event(async_finish)
+                            self._g.timeout_s, int(num_worst_tokens))
+            return r[0], None, None, None, None
         if is_token_in_rank is None:
             raise ConfigError("is_token_in_rank is required without a handle")
         r = X.dispatch1(self._native, xd, xs, is_token_in_rank, num_tokens_per_expert, topk_idx, topk_weights,
-                        expert_alignment, self._sms(config), self._g.timeout_s)
-        return r[0], r[1], r[2], r[3], r[4], _event(async_finish)
+                        expert_alignment, self._sms(config), self._g.timeout_s, int(num_worst_tokens))
+        return r[0], r[1], r[2], r[3], r[4]
 
     def combine(self, x: torch.Tensor, handle: tuple, topk_weights: Optional[torch.Tensor] = None,
                 bias=None, config: Optional[Config] = None, previous_event: Optional[EventOverlap] = None,
                 async_finish: bool = False, allocate_on_comm_stream: bool = False):
         if bias is not None:
             raise UnsupportedOperation("combine bias is not supported")
-        if previous_event is not None:
-            previous_event.current_stream_wait()
-        if self.ht_transport == "ring":
-            ((out, out_w),) = self._g.combine([x], [handle], [topk_weights], config)
-            return out, out_w, _event(async_finish)
-        out, out_w = X.combine1(self._native, x, handle, topk_weights, self._sms(config))
-        return out, out_w, _event(async_finish)
+        with _CommStream(self, previous_event, async_finish, allocate_on_comm_stream, (x, topk_weights)) as cs:
+            if self.ht_transport == "ring":
+                ((out, out_w),) = self._g.combine([x], [handle], [topk_weights], config)
+            else:
+                out, out_w = X.combine1(self._native, x, handle, topk_weights, self._sms(config))
+            ev = cs.finish((out, out_w))
+        return out, out_w, ev
 
     # -- low-latency mode -----------------------------------------------------------
     def low_latency_dispatch(self, x: torch.Tensor, topk_idx: torch.Tensor, num_max_dispatch_tokens_per_rank: int,
@@ -442,12 +531,14 @@ class Buffer:
             raise ConfigError("Buffer was not created with low_latency_mode=True")
         if use_ue8m0:
             raise UnsupportedOperation("UE8M0-packed scales are not supported; use round_scale=True for pow2 scales")
-        res, hook = self._g.ll_dispatch([x], [topk_idx], num_max_dispatch_tokens_per_rank, num_experts, use_fp8,
-                                        round_scale, return_recv_hook, self.ll_transport == "proxy")
-        recv, count, handle = res[0]
-        if cumulative_local_expert_recv_stats is not None:
-            cumulative_local_expert_recv_stats.add_(count)
-        return recv, count, handle, _event(async_finish), hook
+        with _CommStream(self, None, async_finish, False, (x, topk_idx)) as cs:
+            res, hook = self._g.ll_dispatch([x], [topk_idx], num_max_dispatch_tokens_per_rank, num_experts, use_fp8,
+                                            round_scale, return_recv_hook, self.ll_transport == "proxy")
+            recv, count, handle = res[0]
+            if cumulative_local_expert_recv_stats is not None:
+                cumulative_local_expert_recv_stats.add_(count)
+            ev = cs.finish((recv, count))
+        return recv, count, handle, ev, hook
 
     def low_latency_combine(self, x: torch.Tensor, topk_idx: torch.Tensor, topk_weights: torch.Tensor,
                             handle: tuple, use_logfmt: bool = False, zero_copy: bool = False,
@@ -455,15 +546,32 @@ class Buffer:
                             out: Optional[torch.Tensor] = None):
         if use_logfmt:
             raise UnsupportedOperation("LogFMT combine is not supported")
-        (combined,), hook = self._g.ll_combine([x], [topk_idx], [topk_weights], [handle], return_recv_hook, [out])
-        return combined, _event(async_finish), hook
+        # zero_copy: x may be the tensor get_next_low_latency_combine_buffer returned;
+        # the kernel reads expert outputs wherever they live, so both paths are the same
+        with _CommStream(self, None, async_finish, False, (x, topk_idx, topk_weights)) as cs:
+            (combined,), hook = self._g.ll_combine([x], [topk_idx], [topk_weights], [handle], return_recv_hook,
+                                                   [out])
+            ev = cs.finish((combined,))
+        return combined, ev, hook
 
     def clean_low_latency_buffer(self, num_max_dispatch_tokens_per_rank: int, hidden: int, num_experts: int) -> None:
         """Epoch-stamped flags never need clearing; kept for API compatibility."""
         return None
 
     def get_next_low_latency_combine_buffer(self, handle):
-        raise UnsupportedOperation("zero-copy LL combine buffers are not exposed")
+        """DeepEP zero-copy combine: a [num_local_experts, R*Tmax, hidden] bf16
+        buffer the experts can write into, then passed to
+        low_latency_combine(..., zero_copy=True).  Two buffers alternate per
+        call, like DeepEP's double-buffered low-latency region."""
+        Tm, H, E = int(handle[2]), int(handle[3]), int(handle[4])
+        key = (Tm, H, E)
+        pair = self._ll_comb_bufs.get(key)
+        if pair is None:
+            shape = (E // self.group_size, self.group_size * Tm, H)
+            pair = [[torch.empty(shape, dtype=torch.bfloat16, device=self._rank.device) for _ in range(2)], 0]
+            self._ll_comb_bufs[key] = pair
+        pair[1] ^= 1
+        return pair[0][pair[1]]
 
 
 def exchange_handles(my_handle: bytes, world: int, group=None) -> List[bytes]:
@@ -507,12 +615,13 @@ class LocalGroup:
         return self._g.get_dispatch_layout(topk_idx_list, num_experts)
 
     def dispatch(self, xs, is_token_in_ranks=None, num_tokens_per_experts=None, topk_idxs=None,
-                 topk_weights_list=None, handles=None, expert_alignment=1, config=None):
+                 topk_weights_list=None, handles=None, expert_alignment=1, config=None, num_worst_tokens=0):
         n = self.world
         handles = handles or [None] * n
         none = [None] * n
         return self._g.dispatch(xs, handles, is_token_in_ranks or none, num_tokens_per_experts or none,
-                                topk_idxs or none, topk_weights_list or none, expert_alignment, config)
+                                topk_idxs or none, topk_weights_list or none, expert_alignment, config,
+                                num_worst_tokens)
 
     def combine(self, xs, handles, topk_weights_list=None, config=None):
         return self._g.combine(xs, handles, topk_weights_list, config)

@@ -274,6 +274,8 @@ extern "C" int epb_region(epb_t* ctx, void** base, size_t* bytes) {
   return EPB_OK;
 }
 
+extern "C" int64_t epb_arena_offset(void) { return (int64_t)epb::kRegionHeader; }
+
 extern "C" int epb_trace(epb_t* ctx, int64_t* out64) {
   if (!ctx || !out64) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
   EPB_CUDA(cudaMemcpy(out64, epb::scratch_of(ctx->base)->trace, sizeof(int64_t) * 64, cudaMemcpyDeviceToHost));

@@ -19,7 +19,11 @@
 
 namespace epb {
 
-constexpr int kCombineThreads = 384;  // 12 warps; <= 168 registers/thread
+// Two instantiations (no register spills, no calls on the reduce path):
+//   fan-in <= 1 (one rank: the EP=1 copy path): 16 warps, <= 128 registers;
+//   fan-in <= 8 (every reducer inlined):         8 warps, <= 255 registers.
+constexpr int kCombineThreadsSolo = 512;
+constexpr int kCombineThreads = 256;
 constexpr int kCopyUnroll = 7;
 // ---------------------------------------------------------------------------
 // combine: cooperative grid.  Phase A pushes each received row back into its
@@ -33,8 +37,9 @@ struct CombineParams {
   int phase;                     // proxy: 1 = stage + hand rows to the proxy, 2 = reduce
   int fifo_channels;
   uint64_t ht_calls[kMaxLocal];  // proxy transport: expected ht_sig[1][src]
-  uint32_t epoch[kMaxLocal];
-  uint32_t expected[kMaxLocal];
+  int seg16;                     // reduce work unit: 16-byte columns per (token, segment); 0 = whole rows
+  int bump;                      // this launch ends the call: store the next epoch / done target
+                                 // (device-resident, norm_call_begin/_end; the proxy's stage launch does not)
   RankView rv[kMaxLocal];
   epb_combine_args_t a[kMaxLocal];
   epb_recv_layout_t lay;
@@ -85,16 +90,17 @@ __device__ __forceinline__ void bump_done(const RankView& rv, int d, int me) {
 }
 
 template <int NV>
-__device__ __forceinline__ void reduce_rows(const RowSrc& rs, uint32_t mask, const int32_t* sh, int4* out, int n16,
-                                            int lane) {
-  constexpr int U = NV >= 8 ? 1 : 8 / NV;
+__device__ __forceinline__ void reduce_rows(const RowSrc& rs, uint32_t mask, const int32_t* sh, int4* out, int i0,
+                                            int n16, int lane) {
+  constexpr int U = NV == 1 ? 7 : (NV >= 8 ? 1 : 8 / NV);  // NV = 1: one 224-column segment per lane pass
   const int4* r[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int d = __fns(mask, 0, j + 1);  // (j+1)-th contributing rank, ascending
     r[j] = reinterpret_cast<const int4*>(rs.base[d] + (size_t)(rs.row0[d] + sh[d]) * rs.row_bytes);
   }
-  for (int base = lane; base < n16; base += 32 * U) {
+#pragma unroll 1
+  for (int base = i0 + lane; base < n16; base += 32 * U) {
     int4 v[U][NV];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -118,17 +124,13 @@ __device__ __forceinline__ void reduce_rows(const RowSrc& rs, uint32_t mask, con
   }
 }
 
-// Fan-in >= 2 runs out of line: its own register allocation keeps the
-// kernel body (and the inlined fan-in 1 copy of the EP=1 path) free of spills.
-template <int NV>
-__device__ __noinline__ void reduce_rows_call(const RowSrc& rs, uint32_t mask, const int32_t* sh, int4* out, int n16,
-                                              int lane) {
-  reduce_rows<NV>(rs, mask, sh, out, n16, lane);
+
+__device__ __forceinline__ void zero_row(int4* out, int i0, int n16, int lane) {
+  for (int i = i0 + lane; i < n16; i += 32) st_na_v4(out + i, make_int4(0, 0, 0, 0));
 }
 
-__device__ __forceinline__ void zero_row(int4* out, int n16, int lane) {
-  for (int i = lane; i < n16; i += 32) st_na_v4(out + i, make_int4(0, 0, 0, 0));
-}
+// Work unit of the reduce: a (token, row segment) pair; P.seg16 = 0 means
+// whole rows (the default, measured fastest).
 
 // Phase B: reduce my tokens.  pull: partial d is read in place from d's input
 // (over NVLink); else from my staging, where the sources pushed their rows.
@@ -136,14 +138,14 @@ __device__ __forceinline__ void zero_row(int4* out, int n16, int lane) {
 // overlaps the mode exchange / barrier); blocks with more tokens read global
 constexpr int kShTokens = 64;
 
+template <int kMaxFan>
 __device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bool pull, const int64_t* s_xoff,
                                               const int64_t* s_woff, const int32_t* s_excl, const int32_t* s_mypre,
-                                              const int32_t (*s_sh)[kMaxRanks]) {
+                                              const int32_t (*s_sh)[kMaxRanks], int par) {
   const RankView& rv = P.rv[lr];
   const epb_combine_args_t& a = P.a[lr];
   const int R = rv.world, me = rv.rank, nb = gridDim.x, b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
-  const int par = P.epoch[lr] & 1;
   const int k = a.num_topk;
   const size_t row_bytes = (size_t)a.hidden * 2;
   const int n16 = (int)(row_bytes >> 4);
@@ -171,7 +173,11 @@ __device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bo
   }
   __syncthreads();
   const bool cached = tb1 - tb0 <= kShTokens;
-  for (int t = tb0 + warp; t < tb1; t += nwarps) {
+  const int seg16 = P.seg16 > 0 ? P.seg16 : n16;
+  const int segs = (n16 + seg16 - 1) / seg16;
+  for (int unit = warp; unit < (tb1 - tb0) * segs; unit += nwarps) {
+    const int t = tb0 + unit / segs, sg = unit % segs;
+    const int i0 = sg * seg16, i1 = min(n16, i0 + seg16);
     const int32_t* sh = cached ? s_sh[t - tb0] : a.send_head + (size_t)t * R;
     // contributing ranks as a bitmask; rows are taken in ascending rank order
     // (the canonical sum order) via __fns inside reduce_rows
@@ -180,17 +186,17 @@ __device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bo
     mask = __reduce_or_sync(0xffffffffu, mask);
     int4* out = reinterpret_cast<int4*>(static_cast<char*>(a.combined_x) + (size_t)t * row_bytes);
     switch (__popc(mask)) {
-      case 1: reduce_rows<1>(rs, mask, sh, out, n16, lane); break;
-      case 2: reduce_rows_call<2>(rs, mask, sh, out, n16, lane); break;
-      case 3: reduce_rows_call<3>(rs, mask, sh, out, n16, lane); break;
-      case 4: reduce_rows_call<4>(rs, mask, sh, out, n16, lane); break;
-      case 5: reduce_rows_call<5>(rs, mask, sh, out, n16, lane); break;
-      case 6: reduce_rows_call<6>(rs, mask, sh, out, n16, lane); break;
-      case 7: reduce_rows_call<7>(rs, mask, sh, out, n16, lane); break;
-      case 8: reduce_rows_call<8>(rs, mask, sh, out, n16, lane); break;
-      default: zero_row(out, n16, lane); break;
+      case 1: reduce_rows<1>(rs, mask, sh, out, i0, i1, lane); break;
+      case 2: if constexpr (kMaxFan >= 2) reduce_rows<2>(rs, mask, sh, out, i0, i1, lane); break;
+      case 3: if constexpr (kMaxFan >= 3) reduce_rows<3>(rs, mask, sh, out, i0, i1, lane); break;
+      case 4: if constexpr (kMaxFan >= 4) reduce_rows<4>(rs, mask, sh, out, i0, i1, lane); break;
+      case 5: if constexpr (kMaxFan >= 5) reduce_rows<5>(rs, mask, sh, out, i0, i1, lane); break;
+      case 6: if constexpr (kMaxFan >= 6) reduce_rows<6>(rs, mask, sh, out, i0, i1, lane); break;
+      case 7: if constexpr (kMaxFan >= 7) reduce_rows<7>(rs, mask, sh, out, i0, i1, lane); break;
+      case 8: if constexpr (kMaxFan >= 8) reduce_rows<8>(rs, mask, sh, out, i0, i1, lane); break;
+      default: zero_row(out, i0, i1, lane); break;
     }
-    if (a.combined_topk_weights != nullptr && lane < k) {
+    if (sg == 0 && a.combined_topk_weights != nullptr && lane < k) {
       float w = 0.0f;
       for (uint32_t m = mask; m != 0; m &= m - 1) {
         const int d = __ffs(m) - 1;
@@ -209,10 +215,10 @@ __device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bo
 // my region are sent in place; others are first copied to my send staging.
 __device__ __noinline__ void push_combine_cmds(const CombineParams& P, int lr, const int32_t (*s_cnt)[kMaxRanks],
                                                const int32_t* s_excl, const int32_t* s_sendpre, int64_t x_src,
-                                               int64_t w_src, bool aborted) {
+                                               int64_t w_src, bool aborted, int par) {
   const RankView& rv = P.rv[lr];
   const epb_combine_args_t& a = P.a[lr];
-  const int R = rv.world, me = rv.rank, par = P.epoch[lr] & 1, k = a.num_topk;
+  const int R = rv.world, me = rv.rank, k = a.num_topk;
   const int64_t arena = (int64_t)kRegionHeader, row_bytes = (int64_t)a.hidden * 2;
   for (int s = 0; s < R; ++s) {
     if (s == me) continue;
@@ -237,7 +243,8 @@ __device__ __noinline__ void push_combine_cmds(const CombineParams& P, int lr, c
 }
 
 __device__ __forceinline__ void combine_via_proxy(const CombineParams& P, int lr, const int32_t (*s_cnt)[kMaxRanks],
-                                                  const int32_t* s_excl, const int32_t* s_sendpre, bool abort) {
+                                                  const int32_t* s_excl, const int32_t* s_sendpre, bool abort,
+                                                  int par, uint32_t target) {
   const RankView& rv = P.rv[lr];
   const epb_combine_args_t& a = P.a[lr];
   const int R = rv.world, me = rv.rank, nb = gridDim.x, b = blockIdx.x;
@@ -286,13 +293,13 @@ __device__ __forceinline__ void combine_via_proxy(const CombineParams& P, int lr
   __syncthreads();
   if (tid == 0) {
     const uint32_t old = atom_add_acq_rel_gpu(&meta_of(rv.base)->comb_done[me], 1u);
-    if (old + 1 == P.expected[lr]) {  // the last of my blocks hands the rows to the proxy
+    if (old + 1 == target) {  // the last of my blocks hands the rows to the proxy
       const int64_t arena = (int64_t)kRegionHeader;
       const int64_t x_src = in_place ? (int64_t)(xp - rv.base) - arena : P.lay.send_off + P.lay.off_x - arena;
       const int64_t w_src = wp == nullptr ? -1
                             : in_place ? (int64_t)(wp - rv.base) - arena
                                        : P.lay.send_off + P.lay.off_topk_w - arena;
-      push_combine_cmds(P, lr, s_cnt, s_excl, s_sendpre, x_src, w_src, abort);
+      push_combine_cmds(P, lr, s_cnt, s_excl, s_sendpre, x_src, w_src, abort, par);
     }
   }
 }
@@ -307,13 +314,13 @@ __global__ void combine_proxy_wait_kernel(const __grid_constant__ CombineParams 
     wait_geq64(rv, &meta_of(rv.base)->ht_sig[1][tid], P.ht_calls[blockIdx.x], 0x320 + tid, 500);
 }
 
-__global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __grid_constant__ CombineParams P) {
+template <int kMaxFan>
+__device__ __forceinline__ void combine_body(const CombineParams& P, uint32_t epoch, uint32_t target) {
   const int lr = blockIdx.y;
   const RankView& rv = P.rv[lr];
   const epb_combine_args_t& a = P.a[lr];
   const int R = rv.world, me = rv.rank, nb = gridDim.x, b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
-  const uint32_t epoch = P.epoch[lr];
   const int par = epoch & 1;
   trace_mark(rv, 15);
   __shared__ int32_t s_sh[kShTokens][kMaxRanks];
@@ -358,11 +365,11 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   __shared__ int64_t s_xoff[kMaxRanks], s_woff[kMaxRanks];
   if (P.proxy) {  // proxy transport: no SM access to peers' memory at all
     if (P.phase == 1) {
-      combine_via_proxy(P, lr, s_cnt, s_excl, s_sendpre, abort);
+      combine_via_proxy(P, lr, s_cnt, s_excl, s_sendpre, abort, par, target);
       trace_mark(rv, 17);
     } else if (!abort) {
       trace_mark_max(rv, 21);
-      reduce_tokens(P, lr, false, s_xoff, s_woff, s_excl, s_mypre, s_sh);
+      reduce_tokens<kMaxFan>(P, lr, false, s_xoff, s_woff, s_excl, s_mypre, s_sh, par);
       trace_mark(rv, 19);
       trace_mark_max(rv, 20);
     }
@@ -432,14 +439,14 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
   // caller reuse the input) while a peer may still be reading it.
   if (!pull || abort) {
     if (tid < R) bump_done(rv, tid, me);
-    if (tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
+    if (tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], target, 0x300 + tid);
     __syncthreads();
   }
   trace_mark(rv, 18);
   trace_mark_max(rv, 21);
   if (abort) return;
 
-  reduce_tokens(P, lr, pull, s_xoff, s_woff, s_excl, s_mypre, s_sh);
+  reduce_tokens<kMaxFan>(P, lr, pull, s_xoff, s_woff, s_excl, s_mypre, s_sh, par);
   trace_mark(rv, 19);
   trace_mark_max(rv, 20);
   if (pull) {
@@ -448,9 +455,19 @@ __global__ void __launch_bounds__(kCombineThreads, 1) combine_kernel(const __gri
       if (tid == 0) atomicAdd(&meta_of(rv.base)->comb_done[0], 1u);
     } else {
       if (tid < R) bump_done(rv, tid, me);
-      if (b == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], P.expected[lr], 0x300 + tid);
+      if (b == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->comb_done[tid], target, 0x300 + tid);
     }
   }
+}
+
+template <int kMaxFan, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) combine_kernel(const __grid_constant__ CombineParams P) {
+  __shared__ uint32_t s_epoch, s_target;
+  if (threadIdx.x == 0) norm_call_begin(P.rv[blockIdx.y], 1, gridDim.x, &s_epoch, &s_target);
+  __syncthreads();
+  const uint32_t epoch = s_epoch, target = s_target;
+  combine_body<kMaxFan>(P, epoch, target);
+  if (threadIdx.x == 0 && P.bump) norm_call_end(P.rv[blockIdx.y], 1, epoch, target);
 }
 
 }  // namespace epb
@@ -471,15 +488,29 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     if (P.proxy && (ctxs[i]->cfg.fifo_channels <= 0 || !ctxs[i]->proxy || ctxs[i]->cfg.ht_transport != EPB_HT_PROXY))
       return epb_set_error(EPB_ERR_CONFIG, "ht_transport=proxy needs FIFO channels and a running proxy on every rank");
   int nb = std::max(1, num_sms / n_local);
-  const int max_active = epb_max_active_blocks((const void*)combine_kernel, kCombineThreads, 0);
+  // one rank (EP=1): every token has fan-in 1 -> the 12-warp copy instantiation
+  const bool solo = ctxs[0]->world == 1;
+  static const bool wide = [] {  // measurement knob: 12-warp multi-rank instantiation (register-capped)
+    const char* v = std::getenv("EPB_COMBINE_WIDE");
+    return v && v[0] == '1';
+  }();
+  const void* kern = solo ? (const void*)combine_kernel<1, kCombineThreadsSolo>
+                     : wide ? (const void*)combine_kernel<8, 384> : (const void*)combine_kernel<8, kCombineThreads>;
+  const int threads = solo ? kCombineThreadsSolo : wide ? 384 : kCombineThreads;
+  // reduce work unit: whole rows (3.5 KB row segments measured slower: EP=2 135
+  // against 124 us, EP=1 22.6 against 21.8 us per combine; profiles/r02_summary.md).
+  // EPB_COMBINE_SEG16 = 16-byte columns per segment (measurement knob).
+  static const int seg_env = [] {
+    const char* v = std::getenv("EPB_COMBINE_SEG16");
+    return v ? std::atoi(v) : -1;
+  }();
+  P.seg16 = seg_env >= 0 ? seg_env : 0;
+  const int max_active = epb_max_active_blocks(kern, threads, 0);
   nb = std::min(nb, std::max(1, max_active * ctxs[0]->num_sms / n_local));
   for (int i = 0; i < n_local; ++i) {
     epb_ctx* c = ctxs[i];
     const epb_combine_args_t& a = args[i];
     if (int e = compute_recv_layout(c, a.hidden, a.num_topk, &P.lay)) return e;
-    P.epoch[i] = ++c->comb_epoch;
-    c->comb_cum += (uint32_t)nb;
-    P.expected[i] = c->comb_cum;
     if (P.proxy) P.ht_calls[i] = ++c->ht_comb_calls;
     P.rv[i] = c->view();
     P.a[i] = a;
@@ -488,15 +519,18 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
   void* kargs[] = {&P};
   if (P.proxy) {  // stage + push | wait for the peers' rows | reduce
     P.phase = 1;
-    EPB_CUDA(cudaLaunchKernel((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
+    P.bump = 0;
+    EPB_CUDA(cudaLaunchKernel(kern, dim3(nb, n_local), dim3(threads), kargs, 0, st));
     combine_proxy_wait_kernel<<<n_local, 32, 0, st>>>(P);
     EPB_CUDA(cudaGetLastError());
     if (!std::getenv("EPB_PROXY_ASYNC")) EPB_CUDA(cudaStreamSynchronize(st));  // see epb_dispatch
     P.phase = 2;
-    EPB_CUDA(cudaLaunchKernel((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
+    P.bump = 1;
+    EPB_CUDA(cudaLaunchKernel(kern, dim3(nb, n_local), dim3(threads), kargs, 0, st));
     return EPB_OK;
   }
-  EPB_CUDA(epb_launch_grid_sync((void*)combine_kernel, dim3(nb, n_local), dim3(kCombineThreads), kargs, 0, st));
+  P.bump = 1;
+  EPB_CUDA(epb_launch_grid_sync(kern, dim3(nb, n_local), dim3(threads), kargs, 0, st));
   return EPB_OK;
 }
 

@@ -55,10 +55,17 @@ struct Meta {
   uint32_t disp_done[kMaxRanks];         // += 1 per dispatch block of src (monotonic)
   uint32_t comb_done[kMaxRanks];         // += 1 per combine block of src (monotonic)
   // LL direct transport: += 1 per sender block of src once its rows (and, for
-  // block 0, the count header) have landed; the receiver resets after use
+  // block 0, the count header) have landed.  Cumulative per parity: the
+  // receiver waits for (calls of this parity so far) x (grid width), so every
+  // rank must keep the same LL grid width for the life of the context
+  // (ll_blocks pins it at the first call)
   uint32_t ll_disp_cnt[2][kMaxRanks];
   uint32_t ll_comb_cnt[2][kMaxRanks];
-  uint64_t proxy_sig[kMaxFifo][kMaxRanks];  // CPU-proxy signals: += 1 per piggybacked WRITE from src on channel
+  // CPU-proxy signals (proxy.cpp): proxy_sig[kind * 32 + t][src] = how many
+  // piggybacked WRITEs src's proxy thread t has landed here, cumulative; kind
+  // 0 = LL dispatch channels, 1 = LL combine channels.  Written with
+  // stream-ordered value stores after the copies they count.
+  uint64_t proxy_sig[kMaxFifo][kMaxRanks];
   uint64_t ht_sig[2][kMaxRanks];         // proxy HT transport: src's ATOMIC += 1 per [dispatch|combine] call
   // combine mode message (tagged words): where src's input rows / weights live
   // inside src's region, in 16-byte / 4-byte units (kNotifyAbort: not there)
@@ -89,6 +96,16 @@ struct Scratch {                         // private to the owning rank
   // can be captured in CUDA graphs and replayed: [dispatch|combine]
   uint32_t ll_epoch[2];
   uint32_t ll_pcnt[2];                   // proxy-transport calls so far (signal targets)
+  // LL proxy transport: arrivals per command group [dispatch|combine][group];
+  // the warp whose arrival completes a group pushes its WRITE and resets it
+  uint32_t llp_grp[2][kMaxFifo];
+  // normal-mode call epochs and cumulative done targets [dispatch|combine],
+  // device-resident so a layout -> dispatch -> combine step can be captured in
+  // a CUDA graph and replayed: each call reads them at kernel start and its
+  // last block (norm_ticket) stores the new values (norm_call_begin / _end)
+  uint32_t norm_epoch[2];
+  uint32_t norm_cum[2];
+  uint32_t norm_ticket[2];
   // GPU -> CPU FIFOs: control arrays live in pinned host memory; the producer
   // keeps its tail (and a cached head) here, in device memory.
   uint64_t fifo_ctl[kMaxFifo];           // device aliases of the pinned ctl arrays
@@ -273,6 +290,26 @@ __device__ __forceinline__ int warp_scan_smem(int32_t* a, int n, int lane, bool 
     }
   }
   return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+// Normal-mode call bookkeeping (Scratch::norm_*).  begin: thread 0 reads the
+// previous call's epoch and cumulative target; every block derives this
+// call's values (epoch + 1, cum + grid width).  end: the last block of the
+// grid (gpu-scope ticket: every block has read the old values by then)
+// stores them for the next call on the stream.
+__device__ __forceinline__ void norm_call_begin(const RankView& rv, int kind, uint32_t grid, uint32_t* epoch,
+                                                uint32_t* target) {
+  Scratch* sc = scratch_of(rv.base);
+  *epoch = *reinterpret_cast<volatile uint32_t*>(&sc->norm_epoch[kind]) + 1u;
+  *target = *reinterpret_cast<volatile uint32_t*>(&sc->norm_cum[kind]) + grid;
+}
+__device__ __forceinline__ void norm_call_end(const RankView& rv, int kind, uint32_t epoch, uint32_t target) {
+  Scratch* sc = scratch_of(rv.base);
+  if (atom_add_acq_rel_gpu(&sc->norm_ticket[kind], 1u) == gridDim.x - 1) {
+    sc->norm_ticket[kind] = 0;
+    *reinterpret_cast<volatile uint32_t*>(&sc->norm_epoch[kind]) = epoch;
+    *reinterpret_cast<volatile uint32_t*>(&sc->norm_cum[kind]) = target;
+  }
 }
 
 // Record an error into the host-visible word (first error wins is not

@@ -20,8 +20,7 @@ struct epb_ctx {
   bool peer_ipc[epb::kMaxRanks] = {};   // opened with cudaIpcOpenMemHandle
   epb::HostInfo* host = nullptr;        // pinned host view
   epb::HostInfo* host_dev = nullptr;    // device alias
-  uint32_t disp_epoch = 0, comb_epoch = 0, ll_disp_epoch = 0, ll_comb_epoch = 0;
-  uint32_t disp_cum = 0, comb_cum = 0;  // cumulative expected block signals per source
+  uint32_t host_seq = 0;                // normal dispatch calls so far: the tag of the host count words
   uint64_t ht_disp_calls = 0, ht_comb_calls = 0;  // proxy transport calls so far (ht_sig targets)
   uint64_t ll_proxy_disp = 0, ll_proxy_comb = 0;  // proxy-transport LL calls so far (signal targets)
   int num_sms = 148;
@@ -34,6 +33,7 @@ struct epb_ctx {
   std::vector<int64_t*> fifo_host;      // ctl arrays (kernels.py:23-31 layout)
   std::vector<int64_t*> fifo_dev;       // device aliases
   epb_proxy* proxy = nullptr;
+  std::vector<int64_t> proxy_trace;     // the last stopped proxy's trace events (4 int64 each)
   epb_barrier_t* barrier = nullptr;     // proxy all-peer barrier (barrier.cpp)
 
   size_t arena_off() const { return epb::kRegionHeader; }
@@ -64,6 +64,9 @@ int epb_max_active_blocks(const void* func, int threads, size_t smem);
 cudaError_t epb_ensure_smem(const void* func, size_t smem);
 void epb_set_carveout(const void* func, bool enable = true);
 bool epb_carveout_skip(const char* name);
+
+// proxy threads a context runs (proxy.cpp): channel c is served by thread c % n
+int epb_proxy_nthreads(const epb_ctx* ctx);
 
 // name of the job-wide barrier segment (barrier.cpp)
 std::string epb_barrier_name(const void* bytes, size_t n);

@@ -76,8 +76,8 @@ struct DispatchParams {
                                 // channel offset, so copies start without waiting for the plan
   int fifo_channels;
   uint64_t ht_calls[kMaxLocal];  // proxy transport: expected ht_sig[0][src] (calls so far)
-  uint32_t epoch[kMaxLocal];   // per-call epoch: the tag of this call's mailbox / host words
-  uint32_t target[kMaxLocal];  // cumulative done target (sum of grid widths so far)
+  uint32_t host_seq[kMaxLocal];  // tag of this call's host words (the host's call counter); the
+                                 // mailbox epoch and done targets are device-resident (norm_call_begin)
   RankView rv[kMaxLocal];
   epb_dispatch_args_t a[kMaxLocal];
   epb_recv_layout_t lay;
@@ -86,11 +86,10 @@ struct DispatchParams {
 // Block 0, warp R + d, at kernel start: my tokens for each of peer d's local
 // experts (known from the inputs alone, so they travel while the channels are
 // being counted; only the peer's host publication needs them).
-__device__ __forceinline__ void post_expert_counts(const DispatchParams& P, int lr, int d) {
+__device__ __forceinline__ void post_expert_counts(const DispatchParams& P, int lr, int d, uint32_t epoch) {
   const RankView& rv = P.rv[lr];
   const epb_dispatch_args_t& a = P.a[lr];
   const int R = rv.world, me = rv.rank, lane = threadIdx.x & 31;
-  const uint32_t epoch = P.epoch[lr];
   NotifyMsg* msg = &meta_of(rv.peer[d])->mbox[epoch & 1][me];
   const int L = a.num_experts > 0 ? a.num_experts / R : 0;
   for (int base = 0; base < L; base += 32 * 8) {  // 8 loads in flight per lane, then the stores
@@ -113,11 +112,10 @@ __device__ __forceinline__ void post_expert_counts(const DispatchParams& P, int 
 // block 0's other warps already copy rows.  All of a thread's words are
 // loaded before any is checked (one round trip when they have all arrived).
 constexpr int kPublishWarps = 2;
-__device__ __forceinline__ void publish_counts(const DispatchParams& P, int lr, int C, bool aborted) {
+__device__ __forceinline__ void publish_counts(const DispatchParams& P, int lr, int C, bool aborted, uint32_t epoch) {
   const RankView& rv = P.rv[lr];
   const epb_dispatch_args_t& a = P.a[lr];
   const int R = rv.world;
-  const uint32_t epoch = P.epoch[lr];
   const int par = epoch & 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int nthr = kPublishWarps * 32;
@@ -145,7 +143,7 @@ __device__ __forceinline__ void publish_counts(const DispatchParams& P, int lr, 
           n += (uint32_t)v[j][s] == epoch ? (int)(v[j][s] >> 32)
                                         : (int)wait_tagged(rv, &my->mbox[par][s].expert_counts[le], epoch, 0x140 + s);
       n = (n + align - 1) / align * align;
-      st_relaxed_sys(&rv.host->notify[1 + le], tagged((uint32_t)n, epoch));
+      st_relaxed_sys(&rv.host->notify[1 + le], tagged((uint32_t)n, P.host_seq[lr]));
     }
   }
   // every source's per-channel counts -> receive channel prefix (handle output)
@@ -182,11 +180,11 @@ __device__ __forceinline__ void publish_counts(const DispatchParams& P, int lr, 
 // blocks.  After the gather only warp 0 is on the critical path (peer
 // messages -> plan); the other warps publish the per-channel words meanwhile.
 __device__ __forceinline__ void exchange_counts(const DispatchParams& P, int lr, int C, int32_t (*s_cnt)[kMaxChannels],
-                                             int32_t (*s_rpm)[kMaxRanks], int32_t* s_slot, int* s_abort) {
+                                             int32_t (*s_rpm)[kMaxRanks], int32_t* s_slot, int* s_abort,
+                                             uint32_t epoch) {
   const RankView& rv = P.rv[lr];
   const epb_dispatch_args_t& a = P.a[lr];
   const int R = rv.world, me = rv.rank;
-  const uint32_t epoch = P.epoch[lr];
   const int par = epoch & 1;
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
   Scratch* sc = scratch_of(rv.base);
@@ -317,6 +315,13 @@ __device__ __forceinline__ void exchange_counts(const DispatchParams& P, int lr,
       rv.host->err_code = err;
     }
   }
+  if (lane == 0 && *s_abort == 0 && a.num_worst_tokens > 0 && s_rpm[R - 1][me] > a.num_worst_tokens) {
+    // more rows than the caller's num_worst_tokens views: the rows still land
+    // inside the slot (capacity is checked above) but the caller cannot see
+    // them all; reported, not aborted (only this rank's sizing is wrong)
+    rv.host->err_detail = ((int64_t)s_rpm[R - 1][me] << 8) | me;
+    rv.host->err_code = EPB_ERR_CONFIG;
+  }
   __syncwarp();
   const int ab = *s_abort;
   if (lane < R) {
@@ -333,7 +338,7 @@ __device__ __forceinline__ void exchange_counts(const DispatchParams& P, int lr,
   if (lane == 0) {
     sc->abort = ab;
     // the host sizes its receive tensors from this word (tagged, HostInfo)
-    st_relaxed_sys(&rv.host->notify[0], tagged(ab ? kNotifyAbort : (uint32_t)s_rpm[R - 1][me], epoch));
+    st_relaxed_sys(&rv.host->notify[0], tagged(ab ? kNotifyAbort : (uint32_t)s_rpm[R - 1][me], P.host_seq[lr]));
   }
   trace_mark(rv, 5);
   for (int i = lane; i < R * R; i += 32) a.rank_prefix_matrix[i] = s_rpm[i / R][i % R];
@@ -381,7 +386,6 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   const epb_dispatch_args_t& a = P.a[lr];
   const int R = rv.world, me = rv.rank, C = gridDim.x, c = blockIdx.x, T = a.num_tokens;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
-  const uint32_t epoch = P.epoch[lr];
   Scratch* sc = scratch_of(rv.base);
   extern __shared__ int32_t s_pos[];  // [Tc][R] row of the token inside its channel's run to d, or -1
   __shared__ int32_t s_cnt[kMaxRanks][kMaxChannels];  // block 0: every channel's counts
@@ -392,9 +396,15 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   __shared__ int32_t s_chx[kMaxRanks];
   __shared__ int32_t s_slotv[kMaxRanks], s_base[kMaxRanks], s_mine[kMaxRanks], s_pre[kMaxRanks];
   __shared__ int s_abort;
+  __shared__ uint32_t s_epoch, s_target;
   trace_mark(rv, 0);
-  if (tid == 0) s_abort = 0;
-  if (c == 0 && warp >= R && warp < 2 * R) post_expert_counts(P, lr, warp - R);
+  if (tid == 0) {
+    s_abort = 0;
+    norm_call_begin(rv, 0, gridDim.x, &s_epoch, &s_target);
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch, target = s_target;
+  if (c == 0 && warp >= R && warp < 2 * R) post_expert_counts(P, lr, warp - R, epoch);
 
   // 1. channel-relative positions and per-(destination, channel) counts
   // channel c = a contiguous token range (solo: channel 0 is empty, the
@@ -419,7 +429,7 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   // 2. block 0 exchanges counts with the peers and publishes the plan; the
   //    other blocks read their part of it (tagged words, one warp polls)
   if (c == 0) {
-    exchange_counts(P, lr, C, s_cnt, s_rpm, s_slot, &s_abort);
+    exchange_counts(P, lr, C, s_cnt, s_rpm, s_slot, &s_abort, epoch);
     __syncthreads();
   }
   if (P.perblock && c > 0) {
@@ -553,7 +563,7 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
 
   // 3. push rows (block 0's first warps publish the counts meanwhile)
   const int first_copy_warp = c == 0 ? kPublishWarps : 0;
-  if (warp < first_copy_warp) publish_counts(P, lr, C, s_abort != 0);
+  if (warp < first_copy_warp) publish_counts(P, lr, C, s_abort != 0, epoch);
   if (!s_abort) {
     for (int i = tid; i < nt * R; i += blockDim.x) {  // handle: row of t inside my block at d, or -1
       const int p = s_pos[i];
@@ -563,28 +573,49 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     const int n16 = (int)(row_bytes >> 4);
     const int k = a.num_topk, S = a.num_scales;
     const int L = (a.topk_idx != nullptr && a.num_experts > 0) ? a.num_experts / R : 0;
-    for (int tt = warp - first_copy_warp; !P.notify_only && tt >= 0 && tt < nt; tt += nwarps - first_copy_warp) {
-      const int t = t0 + tt;
-      const int4* src = reinterpret_cast<const int4*>(static_cast<const char*>(a.x) + (size_t)t * row_bytes);
-      for (int base = 0; base < n16; base += 32 * kCopyUnroll) {
-        int4 v[kCopyUnroll];
+    // Rows move in units of (token, 3.5 KB segment), two units in flight per
+    // warp (14 x 16 B loads per lane): the channel's ~28 tokens x 4 segments
+    // spread evenly over the block's warps (whole rows left the slowest warp
+    // with 2 rows against a mean of 1.75), and each row is read from HBM once
+    // and stored to every destination that needs it.
+    const int wc = warp - first_copy_warp, nwc = nwarps - first_copy_warp;
+    constexpr int kSeg = 32 * kCopyUnroll;
+    const int segs = (n16 + kSeg - 1) / kSeg;
+    const int units = P.notify_only ? 0 : nt * segs;
+    for (int u = wc; wc >= 0 && u < units; u += 2 * nwc) {
+      int4 v[2][kCopyUnroll];
 #pragma unroll
-        for (int u = 0; u < kCopyUnroll; ++u) {
-          const int i = base + u * 32 + lane;
-          if (i < n16) v[u] = ld_nc_v4(src + i);
+      for (int q = 0; q < 2; ++q) {
+        const int uu = u + q * nwc;
+        if (uu >= units) break;
+        const int tt = uu / segs, i0 = (uu % segs) * kSeg;
+        const int4* src = reinterpret_cast<const int4*>(static_cast<const char*>(a.x) + (size_t)(t0 + tt) * row_bytes);
+#pragma unroll
+        for (int j = 0; j < kCopyUnroll; ++j) {
+          const int i = i0 + j * 32 + lane;
+          if (i < n16) v[q][j] = ld_nc_v4(src + i);
         }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int uu = u + q * nwc;
+        if (uu >= units) break;
+        const int tt = uu / segs, i0 = (uu % segs) * kSeg;
         for (int d = 0; d < R; ++d) {
           const int p = s_pos[tt * R + d];
           if (p < 0) continue;
           int4* dst = reinterpret_cast<int4*>(s_dst[d] + P.lay.off_x + (size_t)(s_rb[d] + p) * row_bytes);
 #pragma unroll
-          for (int u = 0; u < kCopyUnroll; ++u) {
-            const int i = base + u * 32 + lane;
-            if (i < n16) st_v4(dst + i, v[u]);
+          for (int j = 0; j < kCopyUnroll; ++j) {
+            const int i = i0 + j * 32 + lane;
+            if (i < n16) st_v4(dst + i, v[q][j]);
           }
         }
       }
-      // per-row metadata: scales, mapped top-k, source index
+    }
+    // per-row metadata: scales, mapped top-k, source index
+    for (int tt = wc; !P.notify_only && wc >= 0 && tt < nt; tt += nwc) {
+      const int t = t0 + tt;
       for (int d = 0; d < R; ++d) {
         const int p = s_pos[tt * R + d];
         if (p < 0) continue;
@@ -621,7 +652,16 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
       if (tid == me) red_release_gpu_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
       else red_release_sys_add(&meta_of(rv.peer[tid])->disp_done[me], 1u);
     }
-    if (c == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->disp_done[tid], P.target[lr], 0x200 + tid);
+    if (c == 0 && a.num_worst_tokens > 0 && a.topk_idx != nullptr && !s_abort) {
+      // num_worst_tokens: receive rows past the real count carry no expert
+      // (DeepEP semantics); block 0 marks them while the peers' rows land
+      const int64_t n_real = (int64_t)s_rpm[R - 1][me] * a.num_topk;
+      const int64_t n_all = (int64_t)a.num_worst_tokens * a.num_topk;
+      int64_t* ti = reinterpret_cast<int64_t*>(rv.base + P.lay.slot0_off + (int64_t)a.recv_slot * P.lay.slot_bytes +
+                                               P.lay.off_topk_idx);
+      for (int64_t i = n_real + tid; i < n_all; i += blockDim.x) ti[i] = -1;
+    }
+    if (c == 0 && tid < R) wait_geq(rv, &meta_of(rv.base)->disp_done[tid], target, 0x200 + tid);
   } else {
     // proxy transport: the last of my blocks to finish hands the peers' rows
     // to the CPU proxy — one WRITE per array and destination (contiguous in
@@ -629,13 +669,14 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     // ht_sig[0][me]; FIFO order on the channel puts the data first
     if (tid == 0) {
       const uint32_t old = atom_add_acq_rel_gpu(&meta_of(rv.base)->disp_done[me], 1u);
-      if (old + 1 == P.target[lr]) push_dispatch_cmds(P, lr, s_slotv, s_base, s_mine, s_pre, s_abort != 0);
+      if (old + 1 == target) push_dispatch_cmds(P, lr, s_slotv, s_base, s_mine, s_pre, s_abort != 0);
     }
     // the peers' rows are awaited by dispatch_proxy_wait_kernel, launched next
     // on the stream: no block of this kernel stays resident spinning on copies
     // the proxy issues (a copy-engine transfer was observed to stall behind one)
   }
   trace_mark(rv, 10);
+  if (tid == 0) norm_call_end(rv, 0, epoch, target);
 }
 
 // Proxy transport: one block per local rank waits until every peer's rows
@@ -700,9 +741,7 @@ static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_a
     return epb_set_error(EPB_ERR_CONFIG, "num_channels x ranks exceeds the co-resident grid; lower num_sms");
   for (int i = 0; i < n_local; ++i) {
     epb_ctx* c = ctxs[i];
-    P.epoch[i] = ++c->disp_epoch;
-    c->disp_cum += (uint32_t)num_channels;
-    P.target[i] = c->disp_cum;
+    P.host_seq[i] = ++c->host_seq;
     if (P.proxy) P.ht_calls[i] = ++c->ht_disp_calls;
     P.rv[i] = c->view();
     P.a[i] = args[i];
@@ -739,7 +778,7 @@ extern "C" int epb_wait_notify(epb_t* ctx, int64_t* num_recv, int32_t* num_recv_
   if (!ctx) return epb_set_error(EPB_ERR_PROTOCOL, "null context");
   if (num_recv_per_expert && (num_local_experts < 0 || num_local_experts > kMaxLocalExperts))
     return epb_set_error(EPB_ERR_PROTOCOL, "num_local_experts out of range");
-  const uint32_t want = ctx->disp_epoch;
+  const uint32_t want = ctx->host_seq;
   const int nwords = 1 + (num_recv_per_expert ? num_local_experts : 0);
   volatile uint64_t* w = ctx->host->notify;
   auto t0 = std::chrono::steady_clock::now();

@@ -168,7 +168,7 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
                   const std::vector<c10::optional<Tensor>>& per_experts,
                   const std::vector<c10::optional<Tensor>>& topk_idxs,
                   const std::vector<c10::optional<Tensor>>& topk_ws, int expert_alignment, int num_channels,
-                  double timeout_s) {
+                  double timeout_s, int num_worst_tokens = 0) {
   const auto t0 = Clock::now();
   const int n = (int)ranks.size();
   const int R = ranks[0]->world, C = num_channels;
@@ -212,6 +212,8 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
       s.E = (int)s.pe.numel();
     }
     s.lay = &ranks[i]->layout(s.H, s.k);
+    if (num_worst_tokens > s.lay->cap_rows)
+      raise_code(EPB_ERR_CONFIG, "num_worst_tokens exceeds the receive slot capacity (num_nvl_bytes)");
     auto lease = ranks[i]->pool->lease();
     s.slot = lease.first;
     s.copy_out = lease.second;
@@ -237,6 +239,7 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
     a.channel_prefix_matrix = hb + R * R;
     a.recv_channel_prefix_matrix = hb + R * R + R * C;
     a.send_head = hb + R * R + 2 * R * C;
+    a.num_worst_tokens = std::max(0, num_worst_tokens);
   }
   cudaStream_t stream = at::cuda::getCurrentCUDAStream().stream();
   auto hs = handles(ranks);
@@ -251,7 +254,7 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
     g_prof.end("dispatch", ev, stream);
     g_ht.t[0] += us_since(t0, t1);
     g_ht.t[1] += us_since(t1, t2);
-    for (int i = 0; i < n && rc == 0; ++i) {
+    for (int i = 0; i < n && rc == 0 && num_worst_tokens <= 0; ++i) {
       const auto tw0 = Clock::now();
       struct Acc {
         Clock::time_point a;
@@ -275,7 +278,9 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
     St& s = st[i];
     Rank& rk = *ranks[i];
     const epb_recv_layout_t& L = *s.lay;
-    const int64_t N = nrecv[i];
+    // num_worst_tokens: no host sync — views of num_worst_tokens rows (rows past
+    // the real count carry recv_topk_idx = -1), no per-expert list (DeepEP)
+    const int64_t N = num_worst_tokens > 0 ? (int64_t)num_worst_tokens : nrecv[i];
     char* slot_base = reinterpret_cast<char*>(rk.base + L.slot0_off + (int64_t)s.slot * L.slot_bytes);
     const at::Device dev = s.x.device();
     auto opts = s.x.options();
@@ -316,7 +321,9 @@ py::list dispatch(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs
     Tensor send_head = hview((int64_t)R * R + 2 * R * C, {s.T, R});
     py::object px = s.xs.defined() ? py::object(py::make_tuple(recv_x, recv_scales)) : py::cast(recv_x);
     py::object lst = py::none();
-    if (s.E) {
+    if (s.E && num_worst_tokens > 0) {
+      lst = py::list();
+    } else if (s.E) {
       const int Lx = s.E / R;
       PyObject* l = PyList_New(Lx);
       if (!l) throw py::error_already_set();
@@ -388,9 +395,10 @@ py::list combine(const std::vector<RankP>& ranks, const std::vector<Tensor>& xs,
 // per-call list packing of the group signatures.
 py::tuple dispatch1(const RankP& rank, const Tensor& x, const c10::optional<Tensor>& x_scales, const Tensor& in_rank,
                     const c10::optional<Tensor>& per_expert, const c10::optional<Tensor>& topk_idx,
-                    const c10::optional<Tensor>& topk_w, int expert_alignment, int num_channels, double timeout_s) {
+                    const c10::optional<Tensor>& topk_w, int expert_alignment, int num_channels, double timeout_s,
+                    int num_worst_tokens) {
   py::list r = dispatch({rank}, {x}, {x_scales}, {in_rank}, {per_expert}, {topk_idx}, {topk_w}, expert_alignment,
-                        num_channels, timeout_s);
+                        num_channels, timeout_s, num_worst_tokens);
   return r[0].cast<py::tuple>();
 }
 

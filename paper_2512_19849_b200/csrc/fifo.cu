@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <cstdint>
+#include <ctime>
 
 #include "ctx.h"
 #include "ll_common.cuh"
@@ -98,6 +100,94 @@ extern "C" int epb_proxy_barrier(epb_t* ctx, int channel, int same_rail, void* s
   return EPB_OK;
 }
 
+namespace epb {
+// Drain(Idx): push DRAIN with length_or_value = Idx + 1 (0 = everything) and
+// block until check_completion(its index).
+__device__ __forceinline__ bool drain_and_wait(const RankView& rv, int ch, int64_t upto) {
+  uint64_t lo, hi;
+  cmd_pack_dev(EPB_CMD_DRAIN, (uint64_t)rv.rank, (uint64_t)ch, 0, 0, upto < 0 ? 0 : (uint64_t)(upto + 1), 0, lo, hi);
+  const int64_t idx = fifo_push(rv, ch, lo, hi);
+  if (idx < 0) return false;
+  uint64_t t0 = 0;
+  int iter = 0;
+  while (!fifo_completed(rv, ch, idx)) {
+    if ((++iter & 255) == 0) {
+      const uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > rv.timeout_ns) {
+        report_error(rv, EPB_ERR_DEADLOCK, 0xb00 + ch);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
+__global__ void proxy_drain_kernel(RankView rv, int ch, int64_t upto) {
+  if (threadIdx.x == 0) drain_and_wait(rv, ch, upto);
+}
+
+// Test producer: n WRITEs on channel ch (block i: src_off + i*bytes -> dst_off + i*bytes
+// at dst), then Drain(first + upto) where first is the index of the first WRITE;
+// once it completes, result[i] = 1 if block i's first and last 16 bytes already
+// match at the destination (only i <= upto is guaranteed), and
+// result[n] = ns from the last push to the drain's completion.
+__global__ void drain_test_kernel(RankView rv, int ch, int dst, int n, int64_t src_off, int64_t dst_off, int64_t bytes,
+                                  int64_t upto, int32_t* result) {
+  if (threadIdx.x != 0) return;
+  int64_t first = -1;
+  for (int i = 0; i < n; ++i) {
+    uint64_t lo, hi;
+    cmd_pack_dev(EPB_CMD_WRITE, (uint64_t)dst, (uint64_t)ch, (uint64_t)(src_off + i * bytes),
+                 (uint64_t)(dst_off + i * bytes), (uint64_t)bytes, 0, lo, hi);
+    const int64_t idx = fifo_push(rv, ch, lo, hi);
+    if (idx < 0) return;
+    if (i == 0) first = idx;
+  }
+  const uint64_t t0 = globaltimer();
+  if (!drain_and_wait(rv, ch, upto < 0 ? -1 : first + upto)) return;
+  const uint64_t t1 = globaltimer();
+  const char* sp = rv.base + kRegionHeader + src_off;
+  const char* dp = rv.peer[dst] + kRegionHeader + dst_off;
+  const int64_t data = (int64_t)rv.region_bytes - (int64_t)kRegionHeader;
+  const bool in_bounds = src_off + n * bytes <= data && dst_off + n * bytes <= data;
+  for (int i = 0; i < n; ++i) {
+    if (!in_bounds) {  // the proxy rejected these WRITEs (FaultError): nothing to compare
+      result[i] = 0;
+      continue;
+    }
+    const int4* a0 = reinterpret_cast<const int4*>(sp + i * bytes);
+    const int4* b0 = reinterpret_cast<const int4*>(dp + i * bytes);
+    const int64_t last = bytes / 16 - 1;
+    const int4 x0 = __ldcv(a0), y0 = __ldcv(b0), x1 = __ldcv(a0 + last), y1 = __ldcv(b0 + last);
+    result[i] = x0.x == y0.x && x0.y == y0.y && x0.z == y0.z && x0.w == y0.w && x1.x == y1.x && x1.y == y1.y &&
+                x1.z == y1.z && x1.w == y1.w;
+  }
+  result[n] = (int32_t)min((uint64_t)INT32_MAX, t1 - t0);
+}
+}  // namespace epb
+
+extern "C" int epb_proxy_drain(epb_t* ctx, int channel, int64_t upto, void* stream) {
+  if (!ctx) return epb_set_error(EPB_ERR_PROTOCOL, "null context");
+  if (channel < 0 || channel >= ctx->cfg.fifo_channels) return epb_set_error(EPB_ERR_CONFIG, "no such FIFO channel");
+  if (!ctx->proxy) return epb_set_error(EPB_ERR_UNSUPPORTED, "proxy not running");
+  epb::proxy_drain_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(ctx->view(), channel, upto);
+  EPB_CUDA(cudaGetLastError());
+  return EPB_OK;
+}
+
+extern "C" int epb_debug_drain_test(epb_t* ctx, int channel, int dst, int n, int64_t src_off, int64_t dst_off,
+                                    int64_t bytes, int64_t upto, int32_t* result, void* stream) {
+  if (!ctx || !result) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
+  if (channel < 0 || channel >= ctx->cfg.fifo_channels || !ctx->proxy)
+    return epb_set_error(EPB_ERR_CONFIG, "no such FIFO channel / proxy not running");
+  if (dst < 0 || dst >= ctx->world || bytes < 16 || bytes % 16) return epb_set_error(EPB_ERR_CONFIG, "bad drain test");
+  epb::drain_test_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(ctx->view(), channel, dst, n, src_off,
+                                                                          dst_off, bytes, upto, result);
+  EPB_CUDA(cudaGetLastError());
+  return EPB_OK;
+}
+
 int epb_proxy_set_count_only(epb_ctx* ctx, bool on);  // proxy.cpp
 
 extern "C" int epb_fifo_device_bench(epb_t* ctx, int64_t num_cmds, int channels, int64_t* elapsed_ns, void* stream) {
@@ -123,11 +213,73 @@ extern "C" int epb_fifo_device_bench(epb_t* ctx, int64_t num_cmds, int channels,
 
 namespace epb {
 __global__ void stamp_kernel(int64_t* dst) { *dst = (int64_t)globaltimer(); }
+
+// Clock calibration: thread 0 stores %globaltimer into a pinned host word in a
+// loop until the host raises *stop (or ~50 ms pass).
+__global__ void clock_beacon_kernel(volatile int64_t* word, volatile int* stop) {
+  const uint64_t t0 = globaltimer();
+  while (!*stop) {
+    const uint64_t t = globaltimer();
+    *word = (int64_t)t;
+    __threadfence_system();
+    if (t - t0 > 50000000ull) break;
+  }
+}
 }  // namespace epb
+
+// Offset between %globaltimer (GPU, ns) and the host's CLOCK_REALTIME (ns):
+// gpu_ns - host_ns, from the sample with the tightest host bracket around a
+// read of the beacon word; *error_ns = half that bracket (plus the PCIe write
+// latency of the beacon, not measured).  Used to put the proxy's host events
+// and the kernels' %globaltimer marks on one time line (tools/trace_ll_proxy.py).
+extern "C" int epb_clock_calibrate(int64_t* offset_ns, int64_t* error_ns) {
+  if (!offset_ns) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
+  int64_t* word = nullptr;
+  int* stop = nullptr;
+  EPB_CUDA(cudaHostAlloc((void**)&word, sizeof(int64_t), cudaHostAllocMapped));
+  EPB_CUDA(cudaHostAlloc((void**)&stop, sizeof(int), cudaHostAllocMapped));
+  *word = 0;
+  *stop = 0;
+  int64_t *dword = nullptr;
+  int* dstop = nullptr;
+  cudaHostGetDevicePointer((void**)&dword, word, 0);
+  cudaHostGetDevicePointer((void**)&dstop, stop, 0);
+  cudaStream_t st;
+  EPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  epb::clock_beacon_kernel<<<1, 1, 0, st>>>(dword, dstop);
+  auto now = []() {
+    timespec ts;
+    clock_gettime(CLOCK_REALTIME, &ts);
+    return (int64_t)ts.tv_sec * 1000000000ll + ts.tv_nsec;
+  };
+  const int64_t deadline = now() + 20000000;
+  while (*(volatile int64_t*)word == 0 && now() < deadline) {
+  }
+  int64_t best = INT64_MAX, off = 0;
+  for (int i = 0; i < 20000; ++i) {
+    const int64_t h0 = now();
+    const int64_t g = *(volatile int64_t*)word;
+    const int64_t h1 = now();
+    if (g != 0 && h1 - h0 < best) {
+      best = h1 - h0;
+      off = g - (h0 + h1) / 2;
+    }
+  }
+  *(volatile int*)stop = 1;
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  cudaFreeHost(word);
+  cudaFreeHost(stop);
+  if (best == INT64_MAX) return epb_set_error(EPB_ERR_CUDA, "clock beacon never ran");
+  *offset_ns = off;
+  if (error_ns) *error_ns = best / 2;
+  return EPB_OK;
+}
 
 extern "C" int64_t epb_debug_ht_sig_offset(void) { return (int64_t)offsetof(epb::Meta, ht_sig); }
 
 extern "C" int epb_debug_stamp(int64_t* dst, void* stream) {
   epb::stamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(dst);
-  return epb_cuda_check(cudaGetLastError(), "stamp");
+  EPB_CUDA(cudaGetLastError());
+  return EPB_OK;
 }

@@ -28,6 +28,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -93,15 +94,97 @@ __device__ __forceinline__ int ordinal_of(const uint32_t* bm_row, int t) {
 }
 
 // ---------------------------------------------------------------------------
+// Proxy transport: command groups.  Group g (< G = disp_channels, one FIFO
+// channel each) owns chunk c = g / R of destination d = g % R's rows (rows
+// [c*n/nc, (c+1)*n/nc) of the n rows for d, nc = chunks of d).  The warp whose
+// arrival completes a group pushes that group's WRITE at once — while other
+// groups are still being produced (token-level GPU-initiated commands,
+// PAPER.md:136-140, :339); nothing waits for the whole grid.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int group_chunks(int G, int R, int d) { return (G - d + R - 1) / R; }
+
+__device__ __forceinline__ int group_of_row(const int32_t* s_g1, int G, int R, int d, int row) {
+  const int nc = group_chunks(G, R, d);
+  for (int c = 0; c < nc; ++c)
+    if (row < s_g1[d + R * c]) return d + R * c;
+  return d + R * (nc - 1);
+}
+
+// Receiver side: piggybacked WRITEs from src's proxy thread pt to me per call
+// (group b goes to rank b % R on channel chan0 + b, served by thread chan % nth).
+__device__ __forceinline__ int proxy_cmds_per_call(int G, int R, int me, int chan0, int nth, int pt) {
+  int n = 0;
+  for (int b = me; b < G; b += R) n += ((chan0 + b) % nth) == pt;
+  return n;
+}
+
+// one thread: wait until every source's proxy threads have landed this call's groups
+__device__ __forceinline__ void wait_proxy_groups(const RankView& rv, const Meta* my, int kind, int G, int half, int R,
+                                                  int me, int nth, uint64_t calls, int64_t tag) {
+  for (int i = threadIdx.x; i < R * nth; i += blockDim.x) {
+    const int s = i / nth, pt = i % nth;
+    const int n = proxy_cmds_per_call(G, R, me, kind ? half : 0, nth, pt);
+    if (n > 0) wait_geq64(rv, &my->proxy_sig[kind * 32 + pt][s], calls * (uint64_t)n, tag + i, 200);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // LL dispatch
 // ---------------------------------------------------------------------------
 struct LLDispatchParams {
-  int n_local, phases, use_proxy, disp_channels;
+  int n_local, phases, use_proxy, disp_channels, pthreads;
+  int ngroups;  // proxy transport: command groups (R x groups per destination, <= disp_channels)
   RankView rv[kMaxLocal];
   epb_ll_dispatch_args_t a[kMaxLocal];
   LLGeom g;
   int64_t ll_off;
 };
+
+// Send-block reuse.  A call writes the send blocks of its parity, which the
+// proxy's copies of the call two back read.  Those copies are complete by
+// causality: this rank's previous call (other parity) could only finish its
+// receive after every peer's previous call pushed, and a peer pushes only
+// after its own receive of the call two back — which waited for this rank's
+// copies to land.  So no wait is needed as long as a call's receive runs
+// before the send of the call two after it (DeepEP's double-buffer rule; the
+// recv hook must be called in time).  Block 0 checks it with ONE read of the
+// channel's COMPLETED word (pinned host memory — a read per block would queue
+// ~150 PCIe reads: measured 125 us) and reports a violation.
+__device__ __forceinline__ void check_channel_backlog(const RankView& rv, int ch) {
+  Scratch* sc = scratch_of(rv.base);
+  const int64_t* ctl = reinterpret_cast<const int64_t*>(sc->fifo_ctl[ch]);
+  const int64_t want = sc->fifo_tail[ch] - 1;  // all but the previous call's command
+  if (want > 0 && ld_acquire_sys(ctl + EPB_CTL_COMPLETED) < want)
+    report_error(rv, EPB_ERR_PROTOCOL, ((int64_t)0x540 << 32) | ch);
+}
+
+// The single lane whose arrival completed dispatch group gid: the chunk-0
+// group also carries d's per-expert count header; then one WRITE with a
+// piggybacked signal on FIFO channel gid (command.py layout, arena offsets).
+__device__ __noinline__ void ll_push_dispatch_group(const LLDispatchParams& P, int lr, int gid, const int32_t* s_g0,
+                                                    const int32_t* s_g1, const int32_t* cnt, uint32_t epoch) {
+  const RankView& rv = P.rv[lr];
+  const LLGeom& g = P.g;
+  const int R = g.R, L = g.L, me = rv.rank, par = epoch & 1;
+  const int d = gid % R, c = gid / R;
+  scratch_of(rv.base)->llp_grp[0][gid] = 0;  // complete: no other arrival this call
+  char* my_ll = rv.base + P.ll_off;
+  const int64_t send_blk = g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
+  if (c == 0) {
+    int32_t* h = reinterpret_cast<int32_t*>(my_ll + send_blk);
+    for (int le = 0; le < L; ++le) h[le] = cnt[d * L + le];
+  }
+  fence_sys();  // the group's rows (acquired through the arrival counter) and the header, before the command
+  const int64_t rel = P.ll_off - (int64_t)kRegionHeader;  // commands address the arena start
+  const int64_t first = c == 0 ? 0 : g.hdr_bytes + (int64_t)s_g0[gid] * g.disp_row;
+  const int64_t len = (c == 0 ? g.hdr_bytes : 0) + (int64_t)(s_g1[gid] - s_g0[gid]) * g.disp_row;
+  const int64_t dst_blk = g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
+  uint64_t lo, hi;
+  cmd_pack_dev(EPB_CMD_WRITE, d, gid, rel + send_blk + first, rel + dst_blk + first, len, EPB_FLAG_PIGGYBACK_ATOMIC,
+               lo, hi);
+  fifo_push(rv, gid, lo, hi);
+  if (rv.trace && gid < 12) scratch_of(rv.base)->trace[40 + gid] = (int64_t)globaltimer();
+}
 
 __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid_constant__ LLDispatchParams P) {
   const int lr = blockIdx.y;
@@ -150,11 +233,77 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     }
     __syncthreads();
     for (int d = warp; d < R; d += nw) warp_scan_smem(pre + d * L, L, lane, true);  // row of expert in dst block
+    // proxy transport: token-major rows per destination (a contiguous token
+    // range is a contiguous row range, so command groups are row ranges)
+    int16_t* s_loc = s_e + (size_t)a.max_tokens * k;  // [T][k] slot of (t, j) among t's rows for d(e); < -1: dup
+    int32_t* rs = reinterpret_cast<int32_t*>(s_loc + (size_t)a.max_tokens * k);  // [R][T+1] first row of t at d
+    __shared__ int32_t s_g0[kMaxFifo], s_g1[kMaxFifo], s_gexp[kMaxFifo];
+    __shared__ uint32_t s_arr[kMaxFifo];  // this block's arrivals per group
+    const int G = P.ngroups;
+    for (int gg = tid; gg < G; gg += blockDim.x) s_arr[gg] = 0;
+    if (P.use_proxy) {
+      if (blockIdx.x == 0 && tid < G) check_channel_backlog(rv, tid);
+      for (int t = tid; t < T; t += blockDim.x) {
+        int u[kMaxRanks];
+#pragma unroll
+        for (int d = 0; d < kMaxRanks; ++d) u[d] = 0;
+        for (int j = 0; j < k; ++j) {
+          const int e = s_e[t * k + j];
+          int loc = -1;
+          if (e >= 0) {
+            int first = j;
+            for (int j2 = 0; j2 < j; ++j2)
+              if (s_e[t * k + j2] == e) {
+                first = j2;
+                break;
+              }
+            if (first == j) {
+              const int d = e / L;
+#pragma unroll
+              for (int dd = 0; dd < kMaxRanks; ++dd)
+                if (dd == d) loc = u[dd]++;
+            } else {
+              loc = -2 - first;
+            }
+          }
+          s_loc[t * k + j] = (int16_t)loc;
+        }
+        for (int d = 0; d < R; ++d) rs[d * (T + 1) + t] = u[d];
+      }
+      for (int d = tid; d < R; d += blockDim.x) rs[d * (T + 1) + T] = 0;
+      __syncthreads();
+      for (int d = warp; d < R; d += nw) warp_scan_smem(rs + d * (T + 1), T + 1, lane, true);
+      __syncthreads();
+      const int NCHc = (H + kChunkCh - 1) / kChunkCh;
+      for (int g = tid; g < G; g += blockDim.x) {
+        const int d = g % R, c = g / R, nc = group_chunks(G, R, d);
+        const int32_t* rd = rs + d * (T + 1);
+        const int n = rd[T];
+        const int r0 = (int)((int64_t)c * n / nc), r1 = (int)((int64_t)(c + 1) * n / nc);
+        int tokens = 0;  // tokens with a row in [r0, r1): each of their items arrives once
+        for (int t = 0; t < T; ++t) tokens += rd[t + 1] > rd[t] && rd[t] < r1 && rd[t + 1] > r0;
+        s_g0[g] = r0;
+        s_g1[g] = r1;
+        s_gexp[g] = tokens * NCHc;
+      }
+      __syncthreads();
+      // empty groups (no rows) still send their WRITE (the header for chunk 0):
+      // every group signals once per call
+      if (blockIdx.x == 0)
+        for (int g = tid; g < G; g += blockDim.x)
+          if (s_gexp[g] == 0) ll_push_dispatch_group(P, lr, g, s_g0, s_g1, cnt, epoch);
+    }
     __syncthreads();
     trace_mark(rv, 25);
 
     const int NCH = (H + kChunkCh - 1) / kChunkCh;
-    for (int item = blockIdx.x * nw + warp; item < T * NCH; item += total_w) {
+    // proxy transport: each block takes a contiguous range of (token, chunk)
+    // items, so it touches few command groups and reports to each of them once
+    const int n_items = T * NCH, ipb = (n_items + gridDim.x - 1) / gridDim.x;
+    const int it0 = P.use_proxy ? blockIdx.x * ipb + warp : blockIdx.x * nw + warp;
+    const int it_end = P.use_proxy ? min(n_items, (int)(blockIdx.x + 1) * ipb) : n_items;
+    const int it_step = P.use_proxy ? nw : total_w;
+    for (int item = it0; item < it_end; item += it_step) {
       const int t = item / NCH, ch = item % NCH;
       // the token's HBM loads first, so their latency overlaps the slot math
       const int ch0 = ch * kChunkCh + lane * 16;
@@ -166,16 +315,29 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
         x1 = ld_nc_v4(src + ch0 / 8 + 1);
       }
       uint64_t p = 0;
+      int gid = -1;  // proxy: the command group of this lane's row
       if (lane < k) {
         const int e = s_e[t * k + lane];
         int32_t slot = -1;
         if (e >= 0) {
           const int d = e / L;
-          const int row = pre[e] + ordinal_of(bm + (size_t)e * W, t);
-          char* blk = P.use_proxy ? my_ll + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block
-                                  : rv.peer[d] + P.ll_off + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
-          p = reinterpret_cast<uint64_t>(blk + g.hdr_bytes + (int64_t)row * rstride);
-          slot = (int32_t)(d * g.rows_per_src + row);
+          if (P.use_proxy) {
+            int loc = s_loc[t * k + lane];
+            const bool dup = loc < -1;  // same expert twice in the token's top-k: one row
+            if (dup) loc = s_loc[t * k + (-2 - loc)];
+            const int row = rs[d * (T + 1) + t] + loc;
+            if (!dup) {
+              p = reinterpret_cast<uint64_t>(my_ll + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block +
+                                             g.hdr_bytes + (int64_t)row * rstride);
+              gid = group_of_row(s_g1, G, R, d, row);
+            }
+            slot = (int32_t)(d * g.rows_per_src + row);
+          } else {
+            const int row = pre[e] + ordinal_of(bm + (size_t)e * W, t);
+            char* blk = rv.peer[d] + P.ll_off + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
+            p = reinterpret_cast<uint64_t>(blk + g.hdr_bytes + (int64_t)row * rstride);
+            slot = (int32_t)(d * g.rows_per_src + row);
+          }
         }
         if (ch == 0) a.comb_slot[(size_t)t * k + lane] = slot;
       }
@@ -198,7 +360,33 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
           }
         }
       }
-      if (ch == 0 && p != 0) *reinterpret_cast<int32_t*>(reinterpret_cast<char*>(p) + meta_off) = t;
+      if (ch == 0 && p != 0) {
+        int32_t* meta = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(p) + meta_off);
+        meta[0] = t;
+        if (P.use_proxy) {  // token-major rows carry their expert and ordinal for the receiver
+          const int e = s_e[t * k + lane];
+          meta[1] = e % L;
+          meta[2] = ordinal_of(bm + (size_t)e * W, t);
+        }
+      }
+      if (P.use_proxy) {  // count this item once at each group it wrote to (block-local)
+        const unsigned act = __ballot_sync(0xffffffffu, gid >= 0);
+        if (gid >= 0) {
+          const unsigned peers = __match_any_sync(act, gid);
+          if (lane == __ffs(peers) - 1) atomicAdd(&s_arr[gid], 1u);
+        }
+      }
+    }
+    if (P.use_proxy) {
+      // the block's rows are stored (bar.sync): report them to their groups,
+      // one gpu-scope acq_rel add per touched group; the add that completes a
+      // group pushes its WRITE at once — no grid-wide ticket on this path
+      __syncthreads();
+      for (int gg = tid; gg < G; gg += blockDim.x) {
+        const uint32_t n = s_arr[gg];
+        if (n && atom_add_acq_rel_gpu(&sc->llp_grp[0][gg], n) + n == (uint32_t)s_gexp[gg])
+          ll_push_dispatch_group(P, lr, gg, s_g0, s_g1, cnt, epoch);
+      }
     }
 
     __shared__ uint32_t s_last;
@@ -225,28 +413,6 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     __syncthreads();
     trace_mark(rv, 27);
     if (s_last && warp == 0) {
-      if (P.use_proxy) {
-        for (int d = 0; d < R; ++d) {
-          char* blk = my_ll + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
-          for (int le = lane; le < L; le += 32) reinterpret_cast<int32_t*>(blk)[le] = cnt[d * L + le];
-        }
-        fence_sys();
-        __syncwarp();
-        if (lane == 0) {
-          for (int d = 0; d < R; ++d) {
-            int rows = 0;
-            for (int le = 0; le < L; ++le) rows += cnt[d * L + le];
-            const int ch = d % P.disp_channels;
-            const int64_t rel = P.ll_off - (int64_t)kRegionHeader;  // commands address the arena start
-            const int64_t src_off = rel + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
-            const int64_t dst_off = rel + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block;
-            const int64_t len = g.hdr_bytes + (int64_t)rows * rstride;
-            uint64_t lo, hi;
-            cmd_pack_dev(EPB_CMD_WRITE, d, ch, src_off, dst_off, len, EPB_FLAG_PIGGYBACK_ATOMIC, lo, hi);
-            fifo_push(rv, ch, lo, hi);
-          }
-        }
-      }
       if (lane == 0) {
         sc->ll_ticket[par] = 0;
         sc->ll_epoch[0] = epoch;
@@ -261,11 +427,13 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     int32_t* s_off = s_hdr + R * L;                       // [R][L] prefix over sources
     int32_t* s_pre = s_off + R * L;                       // [R][L] prefix over experts (row in block)
     int32_t* s_tot = s_pre + R * L;                       // [L + 1] prefix over experts of totals
-    if (tid < R) {
+    int32_t* s_rows = s_tot + L + 1;                      // [R + 1] proxy: prefix over sources of rows
+    if (!P.use_proxy) {
       // cumulative: every call of this parity adds gridDim.x per source (the
       // grid width is pinned per context, epb_ll_dispatch)
-      if (!P.use_proxy) wait_geq(rv, &my_meta->ll_disp_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x600 + tid);
-      else wait_geq64(rv, &my_meta->proxy_sig[me % P.disp_channels][tid], pexp, 0x680 + tid);
+      if (tid < R) wait_geq(rv, &my_meta->ll_disp_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x600 + tid);
+    } else {
+      wait_proxy_groups(rv, my_meta, 0, P.ngroups, P.disp_channels, R, me, P.pthreads, pexp, 0x680);
     }
     __syncthreads();
     trace_mark(rv, 28);
@@ -290,6 +458,14 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       if (s < R) warp_scan_smem(s_pre + s * L, L, lane, true);  // row of (s, le) inside block s
       else warp_scan_smem(s_tot + 1, L, lane, false);            // packed offset of expert le
     }
+    if (P.use_proxy && tid == 0) {
+      int run = 0;
+      for (int s = 0; s < R; ++s) {
+        s_rows[s] = run;
+        for (int le = 0; le < L; ++le) run += s_hdr[s * L + le];
+      }
+      s_rows[R] = run;
+    }
     __syncthreads();
     const int RT = R * g.Tmax;
     if (blockIdx.x == 0) {
@@ -302,15 +478,30 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     const int N = s_tot[L];
     const int pay16 = g.use_fp8 ? H / 16 : H / 8;
     for (int item = blockIdx.x * nw + warp; item < N; item += total_w) {
-      int lo = 0, hi = L;  // find le: s_tot[le] <= item < s_tot[le+1]
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_tot[mid] <= item) lo = mid; else hi = mid;
+      int le, j, s = 0, row;
+      if (P.use_proxy) {
+        // token-major rows: item = (source, row); the row's header names its
+        // expert and its ordinal among the source's tokens for that expert
+        while (s < R - 1 && item >= s_rows[s + 1]) ++s;
+        row = item - s_rows[s];
+        const int32_t* mp = reinterpret_cast<const int32_t*>(my_ll + g.off_disp_recv +
+                                                             (int64_t)(par * R + s) * g.disp_block + g.hdr_bytes +
+                                                             (int64_t)row * rstride + meta_off);
+        int v = 0;
+        if (lane < 2) v = __ldcg(mp + 1 + lane);
+        le = __shfl_sync(0xffffffffu, v, 0);
+        j = s_off[s * L + le] + __shfl_sync(0xffffffffu, v, 1);
+      } else {
+        int lo = 0, hi = L;  // find le: s_tot[le] <= item < s_tot[le+1]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_tot[mid] <= item) lo = mid; else hi = mid;
+        }
+        le = lo;
+        j = item - s_tot[le];
+        while (s < R - 1 && j >= s_off[s * L + le] + s_hdr[s * L + le]) ++s;
+        row = s_pre[s * L + le] + (j - s_off[s * L + le]);
       }
-      const int le = lo, j = item - s_tot[le];
-      int s = 0;
-      while (s < R - 1 && j >= s_off[s * L + le] + s_hdr[s * L + le]) ++s;
-      const int row = s_pre[s * L + le] + (j - s_off[s * L + le]);
       const char* rp = my_ll + g.off_disp_recv + (int64_t)(par * R + s) * g.disp_block + g.hdr_bytes + row * rstride;
       int4* dst = reinterpret_cast<int4*>(static_cast<char*>(a.packed_recv_x) +
                                           ((int64_t)le * RT + j) * (g.use_fp8 ? H : 2 * H));
@@ -331,12 +522,35 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
 // LL combine
 // ---------------------------------------------------------------------------
 struct LLCombineParams {
-  int n_local, phases, use_proxy, disp_channels;
+  int n_local, phases, use_proxy, disp_channels, pthreads;
+  int ngroups;
   RankView rv[kMaxLocal];
   epb_ll_combine_args_t a[kMaxLocal];
   LLGeom g;
   int64_t ll_off;
 };
+
+// The lane whose arrival completed combine group gid (source s = gid % R,
+// chunk gid / R of the rows s sent me): one WRITE of those rows back into s's
+// combine block, piggybacked signal, on FIFO channel disp_channels + gid.
+__device__ __noinline__ void ll_push_combine_group(const LLCombineParams& P, int lr, int gid, const int32_t* s_g0,
+                                                   const int32_t* s_g1, uint32_t epoch) {
+  const RankView& rv = P.rv[lr];
+  const LLGeom& g = P.g;
+  const int R = g.R, me = rv.rank, par = epoch & 1, ch = P.disp_channels + gid;
+  const int s = gid % R;
+  scratch_of(rv.base)->llp_grp[1][gid] = 0;
+  fence_sys();
+  const int64_t rel = P.ll_off - (int64_t)kRegionHeader;
+  const int64_t first = (int64_t)s_g0[gid] * g.comb_row;
+  const int64_t src = rel + g.off_comb_send + (int64_t)(par * R + s) * g.comb_block + first;
+  const int64_t dst = rel + g.off_comb_recv + (int64_t)(par * R + me) * g.comb_block + first;
+  uint64_t lo, hi;
+  cmd_pack_dev(EPB_CMD_WRITE, s, ch, src, dst, (int64_t)(s_g1[gid] - s_g0[gid]) * g.comb_row,
+               EPB_FLAG_PIGGYBACK_ATOMIC, lo, hi);
+  fifo_push(rv, ch, lo, hi);
+  if (rv.trace && gid < 12) scratch_of(rv.base)->trace[52 + gid] = (int64_t)globaltimer();
+}
 
 __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_constant__ LLCombineParams P) {
   const int lr = blockIdx.y;
@@ -363,11 +577,40 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
   if (sending) {
     for (int le = tid; le < L; le += blockDim.x) s_tot[le + 1] = a.packed_recv_count[le];
     if (tid == 0) s_tot[0] = 0;
+    // proxy transport: rows each source sent me (= rows of its combine block),
+    // split into command groups like the dispatch's
+    __shared__ int32_t s_g0[kMaxFifo], s_g1[kMaxFifo], s_ns[kMaxRanks];
+    __shared__ uint32_t s_arr[kMaxFifo];
+    const int G = P.ngroups;
+    for (int gg = tid; gg < G; gg += blockDim.x) s_arr[gg] = 0;
+    if (P.use_proxy) {
+      if (blockIdx.x == 0 && tid < G) check_channel_backlog(rv, P.disp_channels + tid);
+      for (int src = tid; src < R; src += blockDim.x) {
+        int n = 0;
+        for (int le = 0; le < L; ++le) n += (int)(a.packed_recv_layout_range[le * R + src] & 0xffffffffll);
+        s_ns[src] = n;
+      }
+    }
     __syncthreads();
     if (warp == 0) warp_scan_smem(s_tot + 1, L, lane, false);
+    if (P.use_proxy) {
+      for (int gg = tid; gg < G; gg += blockDim.x) {
+        const int src = gg % R, c = gg / R, nc = group_chunks(G, R, src), n = s_ns[src];
+        s_g0[gg] = (int)((int64_t)c * n / nc);
+        s_g1[gg] = (int)((int64_t)(c + 1) * n / nc);
+      }
+      __syncthreads();
+      if (blockIdx.x == 0)  // empty groups still signal once per call
+        for (int gg = tid; gg < G; gg += blockDim.x)
+          if (s_g1[gg] == s_g0[gg]) ll_push_combine_group(P, lr, gg, s_g0, s_g1, epoch);
+    }
     __syncthreads();
     const int N = s_tot[L];
-    for (int item = blockIdx.x * nw + warp; item < N; item += total_w) {
+    const int ipb = (N + gridDim.x - 1) / gridDim.x;  // proxy: contiguous item range per block
+    const int it0 = P.use_proxy ? blockIdx.x * ipb + warp : blockIdx.x * nw + warp;
+    const int it_end = P.use_proxy ? min(N, (int)(blockIdx.x + 1) * ipb) : N;
+    const int it_step = P.use_proxy ? nw : total_w;
+    for (int item = it0; item < it_end; item += it_step) {
       int lo = 0, hi = L;
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -380,6 +623,15 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
                               : rv.peer[s] + P.ll_off + g.off_comb_recv + (int64_t)(par * R + me) * g.comb_block;
       warp_copy<true>(reinterpret_cast<const int4*>(static_cast<const char*>(a.x) + ((int64_t)le * RT + j) * 2 * H),
                       reinterpret_cast<int4*>(blk + (int64_t)row * g.comb_row), n16, lane);
+      if (P.use_proxy && lane == 0) atomicAdd(&s_arr[group_of_row(s_g1, G, R, s, row)], 1u);
+    }
+    if (P.use_proxy) {  // report the block's rows to their groups (see the dispatch)
+      __syncthreads();
+      for (int gg = tid; gg < G; gg += blockDim.x) {
+        const uint32_t n = s_arr[gg];
+        if (n && atom_add_acq_rel_gpu(&sc->llp_grp[1][gg], n) + n == (uint32_t)(s_g1[gg] - s_g0[gg]))
+          ll_push_combine_group(P, lr, gg, s_g0, s_g1, epoch);
+      }
     }
     __shared__ uint32_t s_last;
     __syncthreads();
@@ -388,19 +640,6 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
     if (tid == 0) s_last = atom_add_acq_rel_gpu(&sc->ll_ticket[2 + par], 1u) == gridDim.x - 1;
     __syncthreads();
     if (s_last && warp == 0) {
-      if (P.use_proxy && lane == 0) {
-        for (int s = 0; s < R; ++s) {
-          int64_t rows = 0;
-          for (int le = 0; le < L; ++le) rows += a.packed_recv_layout_range[le * R + s] & 0xffffffffll;
-          const int ch = P.disp_channels + s % P.disp_channels;
-          const int64_t rel = P.ll_off - (int64_t)kRegionHeader;  // commands address the arena start
-          const int64_t src_off = rel + g.off_comb_send + (int64_t)(par * R + s) * g.comb_block;
-          const int64_t dst_off = rel + g.off_comb_recv + (int64_t)(par * R + me) * g.comb_block;
-          uint64_t lo, hi;
-          cmd_pack_dev(EPB_CMD_WRITE, s, ch, src_off, dst_off, rows * g.comb_row, EPB_FLAG_PIGGYBACK_ATOMIC, lo, hi);
-          fifo_push(rv, ch, lo, hi);
-        }
-      }
       if (lane == 0) {
         sc->ll_ticket[2 + par] = 0;
         sc->ll_epoch[1] = epoch;
@@ -425,9 +664,10 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
         pre_w[q] = a.topk_weights[(size_t)t * k + lane];
       }
     }
-    if (tid < R) {
-      if (!P.use_proxy) wait_geq(rv, &my_meta->ll_comb_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x700 + tid);
-      else wait_geq64(rv, &my_meta->proxy_sig[P.disp_channels + me % P.disp_channels][tid], pexp, 0x780 + tid);
+    if (!P.use_proxy) {
+      if (tid < R) wait_geq(rv, &my_meta->ll_comb_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x700 + tid);
+    } else {
+      wait_proxy_groups(rv, my_meta, 1, P.ngroups, P.disp_channels, R, me, P.pthreads, pexp, 0x780);
     }
     __syncthreads();
     trace_mark(rv, 34);
@@ -558,11 +798,27 @@ static int ll_blocks(epb_t* const* ctxs, int n_local, int num_sms, const void* k
   return pinned <= cap ? pinned : 0;
 }
 
-static int ll_transport(epb_ctx* c, int use_proxy, int* disp_channels) {
+// Command groups per destination rank for the proxy transport (EPB_LL_GROUPS_PER_RANK,
+// default 1): each group is one WRITE the proxy turns into one cudaMemcpyAsync, which
+// costs the host 3-6 us (profiles/r02_ll_proxy.md), so finer groups only pay when the
+// copies are large enough to overlap that cost.
+static int ll_groups(int world, int disp_channels) {
+  static const int per = [] {
+    const char* s = std::getenv("EPB_LL_GROUPS_PER_RANK");
+    return s ? std::max(1, std::atoi(s)) : 1;
+  }();
+  return world * std::max(1, std::min(per, disp_channels / std::max(1, world)));
+}
+
+static int ll_transport(epb_ctx* c, int use_proxy, int* disp_channels, int* pthreads) {
+  *pthreads = 1;
   if (use_proxy) {
     if (c->cfg.fifo_channels < 2 || !c->proxy)
       return epb_set_error(EPB_ERR_UNSUPPORTED, "proxy transport needs >= 2 FIFO channels and a running proxy");
-    *disp_channels = c->cfg.fifo_channels / 2;
+    *disp_channels = c->cfg.fifo_channels / 2;  // one command group per channel, dispatch and combine halves
+    if (*disp_channels < c->world)
+      return epb_set_error(EPB_ERR_CONFIG, "LL proxy transport needs fifo_channels >= 2 x world (a group per rank)");
+    *pthreads = epb_proxy_nthreads(c);
   } else {
     *disp_channels = std::max(1, c->cfg.fifo_channels / 2);
   }
@@ -585,13 +841,16 @@ extern "C" int epb_ll_dispatch(epb_t* const* ctxs, int n_local, const epb_ll_dis
     epb_ctx* c = ctxs[i];
     if (int e = ll_check(c, P.g)) return e;
     if (args[i].num_tokens > args[i].max_tokens) return epb_set_error(EPB_ERR_CONFIG, "num_tokens exceeds max_tokens");
-    if (int e = ll_transport(c, P.use_proxy, &P.disp_channels)) return e;
+    if (int e = ll_transport(c, P.use_proxy, &P.disp_channels, &P.pthreads)) return e;
+    P.ngroups = ll_groups(c->world, P.disp_channels);
     P.rv[i] = c->view();
     P.a[i] = args[i];
   }
   const int W = std::max(1, (a0.max_tokens + 31) / 32);
-  const size_t smem_send = ((size_t)P.g.E * W + 2 * P.g.E) * 4 + (size_t)a0.max_tokens * a0.num_topk * 2;
-  const size_t smem_recv = (size_t)(3 * P.g.R * P.g.L + P.g.L + 1) * 4;
+  size_t smem_send = ((size_t)P.g.E * W + 2 * P.g.E) * 4 + (size_t)a0.max_tokens * a0.num_topk * 2;
+  if (P.use_proxy)  // token-major slots [T][k] int16 + first row per (destination, token)
+    smem_send += (size_t)a0.max_tokens * a0.num_topk * 2 + (size_t)P.g.R * (a0.max_tokens + 1) * 4;
+  const size_t smem_recv = (size_t)(3 * P.g.R * P.g.L + P.g.L + 1 + P.g.R + 1) * 4;
   const size_t smem = std::max(smem_send, smem_recv);
   if (smem > 200 * 1024) return epb_set_error(EPB_ERR_CONFIG, "LL dispatch shape needs too much shared memory");
   epb_set_carveout((const void*)ll_dispatch_kernel);
@@ -620,7 +879,8 @@ extern "C" int epb_ll_combine(epb_t* const* ctxs, int n_local, const epb_ll_comb
   for (int i = 0; i < n_local; ++i) {
     epb_ctx* c = ctxs[i];
     if (int e = ll_check(c, P.g)) return e;
-    if (int e = ll_transport(c, P.use_proxy, &P.disp_channels)) return e;
+    if (int e = ll_transport(c, P.use_proxy, &P.disp_channels, &P.pthreads)) return e;
+    P.ngroups = ll_groups(c->world, P.disp_channels);
     P.rv[i] = c->view();
     P.a[i] = args[i];
   }

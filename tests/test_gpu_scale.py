@@ -148,8 +148,9 @@ def test_dsv3_ll_ep8_full_size(torch, transport):
     grp, xs, idxs, ws, res, Tmax = _ll_case(torch, R, T, H, E, k, True, seed=13, transport=transport)
     try:
         out, comb_slots = _check_ll_dispatch(torch, R, E, xs, idxs, res, Tmax, True)
-        for d in range(R):
-            assert np.array_equal(res[d][2][6].cpu().numpy(), comb_slots[d])
+        if transport == "nvlink":  # proxy rows are token-major: different (internal) combine slots
+            for d in range(R):
+                assert np.array_equal(res[d][2][6].cpu().numpy(), comb_slots[d])
         L = E // R
         gen = torch.Generator(device="cuda")
         gen.manual_seed(13)

@@ -37,7 +37,7 @@ def _rows_equal(torch, got, src, toks_np):
     return torch.equal(got.contiguous().view(torch.uint8), exp.contiguous().view(torch.uint8))
 
 
-def verify_normal(torch, rank, R, E, inputs, res, comb, *, fp8_cast=None, check_tokens=None):
+def verify_normal(torch, rank, R, E, inputs, res, comb, *, fp8_cast=None, check_tokens=None, check_per_expert=True):
     """inputs(s) -> (x bf16, idx, w): source s's tokens and routing; fp8_cast:
     the FP8 cast the dispatch input went through (None for bf16 dispatch).  res: this rank's Buffer.dispatch result
     (recv_x, topk_idx, topk_w, per-expert list, handle); comb: (combined_x,
@@ -67,7 +67,8 @@ def verify_normal(torch, rank, R, E, inputs, res, comb, *, fp8_cast=None, check_
     if ti is not None:
         assert np.array_equal(ti.cpu().numpy(), o["recv_topk_idx"]), "recv_topk_idx"
         assert np.array_equal(tw.cpu().numpy(), o["recv_topk_weights"]), "recv_topk_weights"
-        assert per_exp == o["num_recv_per_expert"], "num_recv_tokens_per_expert"
+        if check_per_expert:
+            assert per_exp == o["num_recv_per_expert"], "num_recv_tokens_per_expert"
     assert np.array_equal(handle[3].cpu().numpy(), o["recv_src_idx"]), "recv_src_idx"
     assert np.array_equal(handle[0].cpu().numpy(), rpm), "rank_prefix_matrix"
     assert np.array_equal(handle[5].cpu().numpy(), heads[rank]), "send_head"
@@ -126,7 +127,8 @@ def verify_ll(torch, rank, R, E, Tmax, inputs, ys, recv, count, handle, combined
         if n:
             assert np.array_equal(q[le, :n], ob["x"]), ("fp8 rows", le)
             assert np.array_equal(sc[le, :n], ob["scales"]), ("scales", le)
-    assert np.array_equal(handle[6].cpu().numpy(), comb_slots[rank]), "combine slots"
+    if not handle[9]:  # direct transport: expert-major rows, the oracle's slots (proxy rows are token-major)
+        assert np.array_equal(handle[6].cpu().numpy(), comb_slots[rank]), "combine slots"
     expert_outs = []
     for d in range(R):
         y = ys(d)
