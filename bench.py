@@ -123,6 +123,59 @@ class Clocks:
                 "samples": len(self.samples), "source": "NVML during the timed region"}
 
 
+class NvlinkGpm:
+    """NVLink bytes from NVML GPM (GPU Performance Monitoring) samples: the
+    device's total NVLink TX / RX bandwidth between two samples, times the
+    interval (nvidia-smi's nvlink throughput counters read N/A on this pool)."""
+
+    def __init__(self, index: int):
+        self.ok, self.source = False, "unavailable"
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            if not nv.nvmlGpmQueryDeviceSupport(self.h).isSupportedDevice:
+                self.source = "GPM not supported"
+                return
+            self.s1, self.s2 = nv.nvmlGpmSampleAlloc(), nv.nvmlGpmSampleAlloc()
+            self.ok, self.source = True, "NVML GPM NVLINK_TOTAL_{TX,RX}_PER_SEC (MiB/s) x interval"
+        except Exception as exc:  # noqa: BLE001
+            self.source = f"unavailable: {type(exc).__name__}: {exc}"[:120]
+
+    def start(self):
+        if self.ok:
+            try:
+                self.nv.nvmlGpmSampleGet(self.h, self.s1)
+            except Exception as exc:  # noqa: BLE001  (e.g. GPM not permitted in this container)
+                self.ok, self.source = False, f"unavailable: nvmlGpmSampleGet: {exc}"[:120]
+            self.t0 = time.perf_counter()
+
+    def stop(self):
+        if not self.ok:
+            return None, None
+        nv = self.nv
+        try:
+            nv.nvmlGpmSampleGet(self.h, self.s2)
+        except Exception as exc:  # noqa: BLE001
+            self.ok, self.source = False, f"unavailable: nvmlGpmSampleGet: {exc}"[:120]
+            return None, None
+        dt = time.perf_counter() - self.t0
+        mg = nv.c_nvmlGpmMetricsGet_t()
+        mg.version = nv.NVML_GPM_METRICS_GET_VERSION
+        mg.numMetrics = 2
+        mg.sample1, mg.sample2 = self.s1, self.s2
+        mg.metrics[0].metricId = nv.NVML_GPM_METRIC_NVLINK_TOTAL_TX_PER_SEC
+        mg.metrics[1].metricId = nv.NVML_GPM_METRIC_NVLINK_TOTAL_RX_PER_SEC
+        try:
+            nv.nvmlGpmMetricsGet(mg)
+        except Exception:  # noqa: BLE001
+            return None, None
+        if mg.metrics[0].nvmlReturn or mg.metrics[1].nvmlReturn:
+            return None, None
+        return mg.metrics[0].value * (1 << 20) * dt, mg.metrics[1].value * (1 << 20) * dt
+
+
 # ----------------------------------------------------------------------------------
 # CPU reference arm (the oracle port; /root/reference does not exist on the GPU box)
 # ----------------------------------------------------------------------------------
@@ -245,7 +298,7 @@ def run_ours(args):
     nvl = epb.nvl_bytes_hint(T_PER_RANK, HIDDEN, R, TOPK, NSLOTS)
     ll_bytes = epb.Buffer.get_low_latency_rdma_size_hint(LL_TOKENS, HIDDEN, R, EXPERTS, num_topk=TOPK)
     buf = epb.Buffer(group, nvl, ll_bytes, low_latency_mode=True, num_recv_slots=NSLOTS, fifo_channels=16,
-                     fifo_capacity=1024, proxy_threads=4, ll_transport="nvlink")
+                     fifo_capacity=1024, ll_transport="nvlink")
 
     # rotating input sets (4 x 58.7 MB > 126 MB L2); seeded so any rank can
     # regenerate any other rank's set (oracle verification, tests/verify.py)
@@ -392,20 +445,76 @@ def run_ours(args):
     del graphs
     barrier()
 
-    # per-kernel device times: graphs with external event nodes between the ops
-    pgraphs = capture(True)
-    for i in range(NSETS):
-        pgraphs[i][0].replay()
+    # per-kernel device times: one graph per op kind, replayed back to back (the
+    # layout / dispatch outputs they read are fixed), CUDA events around K
+    # replays on the replaying stream; avg launch = elapsed / K.  The same loops,
+    # run longer, are bracketed by NVML GPM samples (NVLink TX/RX bytes, N > 1).
+    kgraphs = {}
+    with torch.cuda.stream(cap_stream):
+        cap_stream.wait_stream(torch.cuda.current_stream())
+        fixed = []
+        for i in range(NSETS):
+            x, idx, w = sets[i]
+            pr, _, pe, ir, _ = buf.get_dispatch_layout(idx, EXPERTS)
+            fixed.append((x, idx, w, pr, pe, ir))
+        rx0, _, rtw0, _, h0, _ = buf.dispatch(sets[0][0], num_tokens_per_rank=fixed[0][3], is_token_in_rank=fixed[0][5],
+                                              num_tokens_per_expert=fixed[0][4], topk_idx=sets[0][1],
+                                              topk_weights=sets[0][2], num_worst_tokens=n_worst)
+        buf.combine(rx0, h0, topk_weights=rtw0)
+        cap_stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        for kind in ("layout", "dispatch"):
+            gl = []
+            for i in range(NSETS):
+                g = torch.cuda.CUDAGraph()
+                x, idx, w, pr, pe, ir = fixed[i]
+                with torch.cuda.graph(g, stream=cap_stream):
+                    if kind == "layout":
+                        keep = buf.get_dispatch_layout(idx, EXPERTS)
+                    else:
+                        keep = buf.dispatch(x, num_tokens_per_rank=pr, is_token_in_rank=ir, num_tokens_per_expert=pe,
+                                            topk_idx=idx, topk_weights=w, num_worst_tokens=n_worst)
+                gl.append((g, keep))
+            kgraphs[kind] = gl
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap_stream):
+            keep = buf.combine(rx0, h0, topk_weights=rtw0)
+        kgraphs["combine"] = [(g, keep)]
+    torch.cuda.current_stream().wait_stream(cap_stream)
     barrier()
-    per_kernel = {"layout": [], "dispatch": [], "combine": []}
-    for i in range(args.steps):
-        g, _, _, ev = pgraphs[i % NSETS]
-        g.replay()
-        torch.cuda.synchronize()
-        per_kernel["layout"].append(ev[0].elapsed_time(ev[1]))
-        per_kernel["dispatch"].append(ev[1].elapsed_time(ev[2]))
-        per_kernel["combine"].append(ev[2].elapsed_time(ev[3]))
-    del pgraphs
+
+    def kernel_loop(kind, n):
+        gl = kgraphs[kind]
+        for j in range(n):
+            gl[j % len(gl)][0].replay()
+
+    per_kernel = {}
+    for kind in ("layout", "dispatch", "combine"):
+        kernel_loop(kind, 3)
+        barrier()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record()
+        kernel_loop(kind, args.steps)
+        k1.record()
+        barrier()
+        per_kernel[kind] = [max_over_ranks(k0.elapsed_time(k1)) / args.steps]
+    nvlink = None
+    if R > 1:
+        gpm = NvlinkGpm(local_rank)
+        nvlink = {"source": gpm.source}
+        for kind in ("dispatch", "combine"):
+            reps = max(200, int(0.25 / max(1e-6, per_kernel[kind][0] / 1e3)))  # >= 0.25 s per GPM interval
+            barrier()
+            gpm.start()
+            kernel_loop(kind, reps)
+            torch.cuda.synchronize()
+            tx, rx = gpm.stop()
+            barrier()
+            if tx is not None:
+                nvlink[kind] = {"tx_bytes_per_launch": int(tx / reps), "rx_bytes_per_launch": int(rx / reps),
+                                "launches": reps}
+    del kgraphs
     barrier()
 
     # ---- roofline of the dominant kernel -------------------------------------------------
@@ -423,7 +532,9 @@ def run_ours(args):
     achieved = algo / (avg[dom] / 1e3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
+    if R > 1 and nvlink and nvlink.get(dom):
+        traffic = nvlink[dom]["tx_bytes_per_launch"]  # NVLink bytes this GPU sent per launch (GPM, live)
+    elif tp.exists():
         try:
             traffic = json.loads(tp.read_text()).get(f"{dom}_ep{R}")
         except Exception:
@@ -432,7 +543,9 @@ def run_ours(args):
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind if R == 1 else
                 "B200_PROFILING.md measured peer copy (770 GB/s/direction)",
                 "algorithmic_bytes_per_launch": int(algo), "avg_launch_ms": round(avg[dom], 4),
-                "timing": "CUDA events (external graph nodes) around the kernel inside the replayed step graph"}
+                "timing": "CUDA events around K back-to-back replays of a one-kernel graph (fixed inputs)",
+                "traffic_source": ("NVML GPM NVLink TX during the kernel's replay loop" if R > 1
+                                   else "ncu --set full capture (profiles/traffic.json)")}
     kernels_ms = {k: round(v, 4) for k, v in avg.items()}
 
     # ---- end to end from pinned host buffers ---------------------------------------------
@@ -552,7 +665,7 @@ def run_ours(args):
                 "verified": {"verified": all(v.get("verified") for v in verified.values()), **verified},
                 "step_mode": f"CUDA graph per step (layout -> dispatch(num_worst_tokens={n_worst}) -> combine), "
                              "replayed back to back",
-                "eager": eager, "kernels_ms": kernels_ms, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
+                "eager": eager, "kernels_ms": kernels_ms, "nvlink_hw": nvlink, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_scope": "per rank",
                 "clocks": clocks.summary(), "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
@@ -621,7 +734,7 @@ def config_bench(name, rank, R, dev, args, barrier, max_over_ranks, group, *, T,
         buf = epb.Buffer(group, epb.ring_nvl_bytes(H, R, TOPK, 74, 64), 0, ht_transport="ring", ring_lanes=74)
     elif own:
         buf = epb.Buffer(group, epb.nvl_bytes_hint(T, H, R, TOPK, 2, ht_proxy=ht == "proxy"), 0, num_recv_slots=2,
-                         fifo_channels=8 if ht == "proxy" else 0, proxy_threads=4, ht_transport=ht)
+                         fifo_channels=8 if ht == "proxy" else 0, ht_transport=ht)
     from tests import verify
 
     def inputs(r):

@@ -94,6 +94,9 @@ int epb_trace(epb_t* ctx, int64_t* out64);
 /* Diagnostics: one thread writes %globaltimer (ns) to the device word *dst, in
    stream order (brackets launches on the same clock as epb_trace's marks). */
 int epb_debug_stamp(int64_t* dst, void* stream);
+/* Diagnostics: LL proxy device state (16 int64: llp_self[2], ll_pcnt[2], ll_epoch[2],
+   llp_grp[0][0..4], llp_grp[1][0..4]). */
+int epb_debug_ll_state(epb_t* ctx, int64_t* out16);
 /* Diagnostics: byte offset of the proxy HT signal counters in a region. */
 int64_t epb_debug_ht_sig_offset(void);
 /* Byte offset of the arena inside a region (TransferCmd offsets are relative to it). */

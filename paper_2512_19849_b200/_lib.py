@@ -173,6 +173,7 @@ _proto("epb_barrier_close", c_int, vp, c_int)
 _proto("epb_proxy_barrier", c_int, vp, c_int, c_int, vp)
 _proto("epb_proxy_drain", c_int, vp, c_int, i64, vp)
 _proto("epb_arena_offset", i64)
+_proto("epb_debug_ll_state", c_int, vp, P64)
 _proto("epb_debug_drain_test", c_int, vp, c_int, c_int, c_int, i64, i64, i64, i64, vp, vp)
 _proto("epb_proxy_trace", i64, vp, P64, i64)
 _proto("epb_clock_calibrate", c_int, P64, P64)
@@ -189,7 +190,7 @@ EXPORTED = [
     "epb_ring_shutdown", "epb_apply_deliveries", "epb_fifo_ctl", "epb_proxy_start", "epb_proxy_stop",
     "epb_proxy_stats", "epb_fifo_device_bench", "epb_barrier_open", "epb_barrier_wait", "epb_barrier_close",
     "epb_proxy_barrier", "epb_proxy_drain", "epb_debug_drain_test", "epb_proxy_trace", "epb_clock_calibrate",
-    "epb_arena_offset",
+    "epb_arena_offset", "epb_debug_ll_state",
 ]
 
 

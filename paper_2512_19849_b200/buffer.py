@@ -131,6 +131,16 @@ def ring_nvl_bytes(hidden: int, num_ranks: int, num_topk: int = 8, lanes: int = 
     return num_ranks * lanes * ring_tokens * (disp + comb)
 
 
+def default_proxy_threads() -> int:
+    """CPU proxy threads per rank when the caller does not choose: the paper's 4
+     when the host has the cores, else what this rank's share of
+    the cores leaves after its main thread (the threads spin while work is in
+    flight, so oversubscribing cores stalls them for scheduler time slices)."""
+    cores = len(os.sched_getaffinity(0))
+    ranks_here = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    return max(1, min(4, cores // max(1, ranks_here) - 1))
+
+
 _HT_CODES = {"nvlink": L.HT_NVLINK, "proxy": L.HT_PROXY, "ring": L.HT_RING}
 
 
@@ -347,7 +357,7 @@ class Buffer:
     def __init__(self, group=None, num_nvl_bytes: int = 0, num_rdma_bytes: int = 0, low_latency_mode: bool = False,
                  num_qps_per_rank: int = 24, allow_nvlink_for_low_latency_mode: bool = True,
                  allow_mnnvl: bool = False, explicitly_destroy: bool = False, *, num_recv_slots: int = 3,
-                 fifo_channels: int = 8, fifo_capacity: int = 1024, proxy_threads: int = 4,
+                 fifo_channels: int = 8, fifo_capacity: int = 1024, proxy_threads: int = 0,
                  ll_transport: str = "nvlink", ht_transport: str = "nvlink", ring_lanes: int = 0):
         import torch.distributed as dist
         if group is not None and dist.is_available() and dist.is_initialized():
@@ -365,7 +375,7 @@ class Buffer:
         self.num_nvl_bytes, self.num_rdma_bytes = int(num_nvl_bytes), int(num_rdma_bytes)
         ll_bytes = self.num_rdma_bytes if low_latency_mode else 0
         self._rank = _Rank(rank, world, max(self.num_nvl_bytes, 1 << 20), ll_bytes, num_recv_slots,
-                           fifo_channels, fifo_capacity, proxy_threads, ht_transport=ht_transport)
+                           fifo_channels, fifo_capacity, proxy_threads or default_proxy_threads(), ht_transport=ht_transport)
         if world > 1:
             h = (C.c_char * L.IPC_HANDLE_BYTES)()
             check(lib.epb_ipc_handle(self._rank.ctx, h))

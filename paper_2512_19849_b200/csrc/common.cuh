@@ -99,6 +99,9 @@ struct Scratch {                         // private to the owning rank
   // LL proxy transport: arrivals per command group [dispatch|combine][group];
   // the warp whose arrival completes a group pushes its WRITE and resets it
   uint32_t llp_grp[2][kMaxFifo];
+  // LL proxy transport, rows to myself: stored straight into my receive block
+  // (no loopback through the proxy); += 1 per completed group [dispatch|combine]
+  uint32_t llp_self[2];
   // normal-mode call epochs and cumulative done targets [dispatch|combine],
   // device-resident so a layout -> dispatch -> combine step can be captured in
   // a CUDA graph and replayed: each call reads them at kernel start and its

@@ -119,10 +119,17 @@ __device__ __forceinline__ int proxy_cmds_per_call(int G, int R, int me, int cha
 }
 
 // one thread: wait until every source's proxy threads have landed this call's groups
+// (my own rows never go through the proxy: they were stored locally and
+// counted on Scratch::llp_self — one add per group, G / R groups per call)
 __device__ __forceinline__ void wait_proxy_groups(const RankView& rv, const Meta* my, int kind, int G, int half, int R,
                                                   int me, int nth, uint64_t calls, int64_t tag) {
   for (int i = threadIdx.x; i < R * nth; i += blockDim.x) {
     const int s = i / nth, pt = i % nth;
+    if (s == me) {
+      if (pt == 0)
+        wait_geq_gpu(rv, &scratch_of(rv.base)->llp_self[kind], (uint32_t)(calls * (uint64_t)(G / R)), tag + i);
+      continue;
+    }
     const int n = proxy_cmds_per_call(G, R, me, kind ? half : 0, nth, pt);
     if (n > 0) wait_geq64(rv, &my->proxy_sig[kind * 32 + pt][s], calls * (uint64_t)n, tag + i, 200);
   }
@@ -150,10 +157,10 @@ struct LLDispatchParams {
 // recv hook must be called in time).  Block 0 checks it with ONE read of the
 // channel's COMPLETED word (pinned host memory — a read per block would queue
 // ~150 PCIe reads: measured 125 us) and reports a violation.
-__device__ __forceinline__ void check_channel_backlog(const RankView& rv, int ch) {
+__device__ __forceinline__ void check_channel_backlog(const RankView& rv, int ch, int64_t keep) {
   Scratch* sc = scratch_of(rv.base);
   const int64_t* ctl = reinterpret_cast<const int64_t*>(sc->fifo_ctl[ch]);
-  const int64_t want = sc->fifo_tail[ch] - 1;  // all but the previous call's command
+  const int64_t want = sc->fifo_tail[ch] - keep;  // all but the newest `keep` commands
   if (want > 0 && ld_acquire_sys(ctl + EPB_CTL_COMPLETED) < want)
     report_error(rv, EPB_ERR_PROTOCOL, ((int64_t)0x540 << 32) | ch);
 }
@@ -167,8 +174,17 @@ __device__ __noinline__ void ll_push_dispatch_group(const LLDispatchParams& P, i
   const LLGeom& g = P.g;
   const int R = g.R, L = g.L, me = rv.rank, par = epoch & 1;
   const int d = gid % R, c = gid / R;
-  scratch_of(rv.base)->llp_grp[0][gid] = 0;  // complete: no other arrival this call
+  Scratch* sc = scratch_of(rv.base);
+  sc->llp_grp[0][gid] = 0;  // complete: no other arrival this call
   char* my_ll = rv.base + P.ll_off;
+  if (d == me) {  // my own rows are already in my receive block: header, then count the group
+    if (c == 0) {
+      int32_t* h = reinterpret_cast<int32_t*>(my_ll + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block);
+      for (int le = 0; le < L; ++le) h[le] = cnt[d * L + le];
+    }
+    red_release_gpu_add(&sc->llp_self[0], 1u);
+    return;
+  }
   const int64_t send_blk = g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
   if (c == 0) {
     int32_t* h = reinterpret_cast<int32_t*>(my_ll + send_blk);
@@ -242,7 +258,6 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     const int G = P.ngroups;
     for (int gg = tid; gg < G; gg += blockDim.x) s_arr[gg] = 0;
     if (P.use_proxy) {
-      if (blockIdx.x == 0 && tid < G) check_channel_backlog(rv, tid);
       for (int t = tid; t < T; t += blockDim.x) {
         int u[kMaxRanks];
 #pragma unroll
@@ -277,14 +292,21 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       const int NCHc = (H + kChunkCh - 1) / kChunkCh;
       for (int g = tid; g < G; g += blockDim.x) {
         const int d = g % R, c = g / R, nc = group_chunks(G, R, d);
-        const int32_t* rd = rs + d * (T + 1);
-        const int n = rd[T];
-        const int r0 = (int)((int64_t)c * n / nc), r1 = (int)((int64_t)(c + 1) * n / nc);
-        int tokens = 0;  // tokens with a row in [r0, r1): each of their items arrives once
-        for (int t = 0; t < T; ++t) tokens += rd[t + 1] > rd[t] && rd[t] < r1 && rd[t + 1] > r0;
-        s_g0[g] = r0;
-        s_g1[g] = r1;
-        s_gexp[g] = tokens * NCHc;
+        const int n = rs[d * (T + 1) + T];
+        s_g0[g] = (int)((int64_t)c * n / nc);
+        s_g1[g] = (int)((int64_t)(c + 1) * n / nc);
+        s_gexp[g] = 0;
+      }
+      __syncthreads();
+      // arrivals a group expects: every item (t, chunk) of each token with a
+      // row in the group arrives once
+      for (int i = tid; i < T * R; i += blockDim.x) {
+        const int t = i / R, d = i % R;
+        const int r_a = rs[d * (T + 1) + t], r_b = rs[d * (T + 1) + t + 1];
+        if (r_b > r_a) {
+          const int g1 = group_of_row(s_g1, G, R, d, r_a), g2 = group_of_row(s_g1, G, R, d, r_b - 1);
+          for (int gg = g1; gg <= g2; gg += R) atomicAdd(&s_gexp[gg], NCHc);
+        }
       }
       __syncthreads();
       // empty groups (no rows) still send their WRITE (the header for chunk 0):
@@ -326,9 +348,10 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
             const bool dup = loc < -1;  // same expert twice in the token's top-k: one row
             if (dup) loc = s_loc[t * k + (-2 - loc)];
             const int row = rs[d * (T + 1) + t] + loc;
-            if (!dup) {
-              p = reinterpret_cast<uint64_t>(my_ll + g.off_disp_send + (int64_t)(par * R + d) * g.disp_block +
-                                             g.hdr_bytes + (int64_t)row * rstride);
+            if (!dup) {  // rows for a peer: my send block; rows for me: my receive block
+              const int64_t blk = d == me ? g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block
+                                          : g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
+              p = reinterpret_cast<uint64_t>(my_ll + blk + g.hdr_bytes + (int64_t)row * rstride);
               gid = group_of_row(s_g1, G, R, d, row);
             }
             slot = (int32_t)(d * g.rows_per_src + row);
@@ -387,6 +410,8 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
         if (n && atom_add_acq_rel_gpu(&sc->llp_grp[0][gg], n) + n == (uint32_t)s_gexp[gg])
           ll_push_dispatch_group(P, lr, gg, s_g0, s_g1, cnt, epoch);
       }
+      // off the critical path: the send-block reuse rule held (one PCIe read)
+      if (blockIdx.x == gridDim.x - 1 && tid >= 32 && tid - 32 < G) check_channel_backlog(rv, tid - 32, 2);
     }
 
     __shared__ uint32_t s_last;
@@ -539,7 +564,12 @@ __device__ __noinline__ void ll_push_combine_group(const LLCombineParams& P, int
   const LLGeom& g = P.g;
   const int R = g.R, me = rv.rank, par = epoch & 1, ch = P.disp_channels + gid;
   const int s = gid % R;
-  scratch_of(rv.base)->llp_grp[1][gid] = 0;
+  Scratch* sc = scratch_of(rv.base);
+  sc->llp_grp[1][gid] = 0;
+  if (s == me) {  // rows returned to myself were stored into my receive block directly
+    red_release_gpu_add(&sc->llp_self[1], 1u);
+    return;
+  }
   fence_sys();
   const int64_t rel = P.ll_off - (int64_t)kRegionHeader;
   const int64_t first = (int64_t)s_g0[gid] * g.comb_row;
@@ -584,7 +614,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
     const int G = P.ngroups;
     for (int gg = tid; gg < G; gg += blockDim.x) s_arr[gg] = 0;
     if (P.use_proxy) {
-      if (blockIdx.x == 0 && tid < G) check_channel_backlog(rv, P.disp_channels + tid);
+
       for (int src = tid; src < R; src += blockDim.x) {
         int n = 0;
         for (int le = 0; le < L; ++le) n += (int)(a.packed_recv_layout_range[le * R + src] & 0xffffffffll);
@@ -619,8 +649,9 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
       const int le = lo, j = item - s_tot[le];
       const int route = a.recv_route[(int64_t)le * RT + j];
       const int s = (int)(route / g.rows_per_src), row = (int)(route % g.rows_per_src);
-      char* blk = P.use_proxy ? my_ll + g.off_comb_send + (int64_t)(par * R + s) * g.comb_block
-                              : rv.peer[s] + P.ll_off + g.off_comb_recv + (int64_t)(par * R + me) * g.comb_block;
+      char* blk = !P.use_proxy ? rv.peer[s] + P.ll_off + g.off_comb_recv + (int64_t)(par * R + me) * g.comb_block
+                  : s == me    ? my_ll + g.off_comb_recv + (int64_t)(par * R + me) * g.comb_block
+                               : my_ll + g.off_comb_send + (int64_t)(par * R + s) * g.comb_block;
       warp_copy<true>(reinterpret_cast<const int4*>(static_cast<const char*>(a.x) + ((int64_t)le * RT + j) * 2 * H),
                       reinterpret_cast<int4*>(blk + (int64_t)row * g.comb_row), n16, lane);
       if (P.use_proxy && lane == 0) atomicAdd(&s_arr[group_of_row(s_g1, G, R, s, row)], 1u);
@@ -632,6 +663,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
         if (n && atom_add_acq_rel_gpu(&sc->llp_grp[1][gg], n) + n == (uint32_t)(s_g1[gg] - s_g0[gg]))
           ll_push_combine_group(P, lr, gg, s_g0, s_g1, epoch);
       }
+      if (blockIdx.x == gridDim.x - 1 && tid >= 32 && tid - 32 < G) check_channel_backlog(rv, P.disp_channels + tid - 32, 2);
     }
     __shared__ uint32_t s_last;
     __syncthreads();

@@ -66,6 +66,7 @@ struct epb_proxy {
   epb_ctx* ctx = nullptr;
   std::vector<std::thread> threads;
   std::atomic<bool> stop{false};
+  std::atomic<int> ready{0};  // threads past their warm-up (epb_proxy_start waits for all)
   std::atomic<bool> count_only{false};
   std::atomic<int64_t> served{0}, copies{0}, atomics{0};
   std::mutex trace_m;
@@ -341,12 +342,20 @@ struct Worker {
     // the first device-to-device copy of a process loads the driver's copy
     // kernel lazily, and that load waited for the LL kernel spinning on the
     // very copy (observed: the first proxy call of a fresh process timed out)
+    // The same holds for the first value write to a peer mapping (its first
+    // LL call stalled for seconds at EP=2 until both paths were warmed here).
     const size_t probe = epb::kMetaBytes + offsetof(epb::Scratch, trace) + sizeof(int64_t) * 62;
     for (int d = 0; d < ctx->world; ++d) {
       if (!ctx->peer[d]) continue;
       DestState& ds = dest(d);
-      if (ok(cudaMemcpyAsync(ctx->peer[d] + probe, ctx->base + probe, 16, cudaMemcpyDefault, ds.st)))
-        ok(cudaStreamSynchronize(ds.st));
+      const size_t big = std::min<size_t>(ctx->cfg.ll_bytes, (size_t)1 << 20);
+      const size_t src = ctx->ll_off(), dst = ctx->ll_off() + (d == ctx->rank ? big : 0);
+      bool good = ok(cudaMemcpyAsync(ctx->peer[d] + probe, ctx->base + probe, 16, cudaMemcpyDefault, ds.st));
+      if (good && big > 0 && d != ctx->rank)  // an LL-sized copy into the peer's (idle) LL region
+        good = ok(cudaMemcpyAsync(ctx->peer[d] + dst, ctx->base + src, big, cudaMemcpyDefault, ds.st));
+      if (good && write_value64())
+        write_value64()(reinterpret_cast<CUstream>(ds.st), reinterpret_cast<CUdeviceptr>(ctx->peer[d] + probe), 0, 0);
+      if (good) ok(cudaStreamSynchronize(ds.st));
     }
     // piggyback counters continue from their device values (proxy restarts)
     for (int d = 0; d < ctx->world; ++d)
@@ -354,6 +363,7 @@ struct Worker {
         const size_t idx = (size_t)(k * 32 + tid) * epb::kMaxRanks + ctx->rank;
         if (ctx->peer[d]) dests[d].sig[k] = seed_counter(d, offsetof(epb::Meta, proxy_sig) + sizeof(uint64_t) * idx);
       }
+    px->ready.fetch_add(1);
     int64_t idle = 0;
     std::vector<std::pair<int, int64_t>> served;
     while (!px->stop.load(std::memory_order_relaxed)) {
@@ -515,6 +525,10 @@ extern "C" int epb_proxy_start(epb_t* ctx) {
   px->ctx = ctx;
   for (int i = 0; i < n; ++i) px->threads.emplace_back(proxy_main, px, i, n);
   ctx->proxy = px;
+  // no kernel may depend on the proxy before its copy paths are warm
+  const auto t0 = std::chrono::steady_clock::now();
+  while (px->ready.load() < n && std::chrono::steady_clock::now() - t0 < std::chrono::seconds(60))
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
   return EPB_OK;
 }
 

@@ -50,7 +50,7 @@ def main():
     from tests.helpers import bf16_random, make_routing
     T, H, E, k = args.tokens, 7168, 256, 8
     buf = epb.Buffer(group, 1 << 20, epb.Buffer.get_low_latency_rdma_size_hint(T, H, world, E, num_topk=k),
-                     low_latency_mode=True, fifo_channels=args.fifo_channels, proxy_threads=4, ll_transport="proxy")
+                     low_latency_mode=True, fifo_channels=args.fifo_channels, ll_transport="proxy")
     g = np.random.default_rng(rank)
     x = torch.from_numpy(bf16_random(g, (T, H)).view(np.int16)).view(torch.bfloat16).cuda()
     idx, w = make_routing(g, T, E, k)
@@ -71,7 +71,19 @@ def main():
         try:
             buf._g.check_device_error()
         except Exception as exc:  # noqa: BLE001  (a timed-out warm-up call: report, keep going)
-            print(f"call {i}: {exc}", file=sys.stderr, flush=True)
+            st = (C.c_int64 * 16)()
+            lib.epb_debug_ll_state(buf._rank.ctx, st)
+            ps = (C.c_int64 * 3)()
+            lib.epb_proxy_stats(buf._rank.ctx, ps)
+            ctl = []
+            for ch in range(args.fifo_channels):
+                q, cap = C.POINTER(C.c_int64)(), C.c_int64()
+                lib.epb_fifo_ctl(buf._rank.ctx, ch, C.byref(q), C.byref(cap))
+                ctl.append((q[0], q[8], q[16]))
+            meta = torch.as_tensor(epb.buffer._SlotMemory(buf._rank.base, 192 + 64 * 64), device="cuda").cpu().numpy()
+            sig = meta[192:].view(np.uint64).reshape(64, 8)
+            print(f"call {i} rank {rank}: {exc}; llp_self/pcnt/epoch/grp {list(st)} proxy {list(ps)} ctl {ctl} "
+                  f"sig disp {sig[:4, :world].tolist()} comb {sig[32:36, :world].tolist()}", file=sys.stderr, flush=True)
             continue
         if i >= 5:
             calls.append(list(m))
@@ -97,7 +109,8 @@ def main():
 
         def rel(v):
             return round((v - t0) / 1e3, 2)
-        return {"staged": rel(m[stage]), "first_push": rel(p0), "last_push": rel(p1),
+        return {"prologue": rel(m[stage - 1]) if start == 24 else None, "staged": rel(m[stage]),
+                "first_push": rel(p0), "last_push": rel(p1),
                 "host_sees_tail": rel(tail[0, 0]) if len(tail) else None,
                 "first_copy_issued": rel(cp[0, 0]) if len(cp) else None,
                 "last_signal_issued": rel(sig[-1, 0]) if len(sig) else None,
@@ -108,13 +121,14 @@ def main():
         near = evs[np.argsort(np.abs(evs[:, 0] - m[24]))[:6]]
         print(f"last call marks start {m[24]} staged {m[26]} wake {m[28]}; nearest host events "
               f"{[(int(e[0] - m[24]), int(e[1])) for e in near]}", file=sys.stderr, flush=True)
-    out = {"rank": rank, "world": world, "tokens": T, "fifo_channels": args.fifo_channels, "groups": G,
+    out = {"rank": rank, "world": world, "tokens": T, "fifo_channels": args.fifo_channels,
+           "groups_per_rank": int(os.environ.get("EPB_LL_GROUPS_PER_RANK", "1")),
            "clock_offset_ns": off.value, "clock_error_ns": err.value, "calls": len(calls)}
     for name, spec in (("dispatch", (24, 26, 40, 28, 29, 0)), ("combine", (32, 33, 52, 34, 35, G))):
         rows = [p for p in (phases(m, *spec) for m in calls) if p]
         med = {}
         for key in rows[0] if rows else []:
-            vals = [r[key] for r in rows if r[key] is not None]
+            vals = [r[key] for r in rows if r.get(key) is not None]
             med[key] = round(statistics.median(vals), 2) if vals else None
         out[name] = med
     line = json.dumps(out)
