@@ -42,7 +42,7 @@ import numpy as np  # noqa: E402
 
 T_PER_RANK, HIDDEN, EXPERTS, TOPK = 4096, 7168, 256, 8
 LL_TOKENS = 128
-NSLOTS = 6  # receive slots: one per captured step graph (4 rotating sets) + eager + the scratch slot
+NSLOTS = 9  # receive slots: the captured step graphs (4 + 3) + eager + the scratch slot
 ROW = HIDDEN * 2
 WORKLOAD = "DeepSeek-V3 normal mode: 4096 tok/rank, hidden 7168, 256 experts, top-8, bf16 dispatch + bf16 combine"
 METRIC = "dispatch/combine GB/s per GPU at 1/2/4/8 B200 (+ LL µs) vs NVLink roofline"
@@ -383,7 +383,10 @@ def run_ours(args):
             ev[3].record()
         return out, (per_rank, per_exp, in_rank, recv_x, rti, rtw, handle, out_w)
 
-    def capture(with_events: bool):
+    def capture(with_events: bool, chains=None):
+        """One graph per input set (chains=None), or one graph per entry of
+        chains: a sequence of consecutive steps (set i, i+1, ...) in one graph,
+        so back-to-back steps need one graph launch per chain."""
         graphs = []
         cap_stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cap_stream):
@@ -392,12 +395,16 @@ def run_ours(args):
             cap_stream.synchronize()
             if world > 1:
                 dist.barrier()
-            for i in range(NSETS):
+            for seq in (chains or [[i] for i in range(NSETS)]):
                 g = torch.cuda.CUDAGraph()
                 ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)] if with_events else None
+                outs, keeps = [], []
                 with torch.cuda.graph(g, stream=cap_stream):
-                    out, keep = graph_step(i, ev)
-                graphs.append((g, out, keep, ev))
+                    for i in seq:
+                        out, keep = graph_step(i, ev)
+                        outs.append(out)
+                        keeps.append(keep)
+                graphs.append((g, outs[0] if len(seq) == 1 else outs, keeps[0] if len(seq) == 1 else keeps, ev))
         torch.cuda.current_stream().wait_stream(cap_stream)
         barrier()
         return graphs
@@ -410,17 +417,31 @@ def run_ours(args):
                                                            EXPERTS))
     barrier()
 
-    # ---- timed region (device events around K graph replays) ------------------------------
+    # ---- timed region (device events around the K steps) --------------------------------
+    # the K steps replay as graphs of NSETS consecutive steps (one graph launch per
+    # 4 steps) plus one graph for the K mod NSETS remaining steps
+    del graphs
+    barrier()
+    n_chain, rem = divmod(args.steps, NSETS)
+    chains = [list(range(NSETS))] + ([list(range(rem))] if rem else [])
+    cgraphs = capture(False, chains)
+    for _ in range(2):
+        cgraphs[0][0].replay()
+    barrier()
     clocks = Clocks(local_rank)
     with clocks:
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        for i in range(args.steps):
-            graphs[i % NSETS][0].replay()
+        for _ in range(n_chain):
+            cgraphs[0][0].replay()
+        if rem:
+            cgraphs[1][0].replay()
         ev1.record()
         barrier()
     ms_local = ev0.elapsed_time(ev1)
+    del cgraphs
+    barrier()
     ms = max_over_ranks(ms_local)
     my_rows = sum(rows[i % NSETS] for i in range(args.steps))
     my_remote = sum(remote_rows[i % NSETS] for i in range(args.steps))
@@ -442,7 +463,6 @@ def run_ours(args):
     ms_eager = max_over_ranks(e0.elapsed_time(e1))
     eager = {"value": round(job_bytes / (ms_eager / 1e3) / 1e9, 3), "ms_per_step": round(ms_eager / args.steps, 4),
              "mode": "eager host launches; the host waits for the receive counts each dispatch"}
-    del graphs
     barrier()
 
     # per-kernel device times: one graph per op kind, replayed back to back (the
@@ -516,6 +536,58 @@ def run_ours(args):
                                 "launches": reps}
     del kgraphs
     barrier()
+
+    # ---- SM budget (the same SMs per GPU as DeepEP) -------------------
+    # dispatch / combine as one-kernel graphs with Config(num_sms=n): n blocks
+    # (channels) for the dispatch, n blocks for the combine; the rest of the GPU
+    # stays free for the caller's compute.
+    sm_budget = {}
+    if not args.no_configs:
+        x0, idx0, w0, pr0, pe0, ir0 = fixed[0]
+        for n_sms in (20, 24, 48):
+            cfg = epb.Config(n_sms)
+            with torch.cuda.stream(cap_stream):
+                cap_stream.wait_stream(torch.cuda.current_stream())
+                rxb, _, rtwb, _, hb, _ = buf.dispatch(x0, num_tokens_per_rank=pr0, is_token_in_rank=ir0,
+                                                      num_tokens_per_expert=pe0, topk_idx=idx0, topk_weights=w0,
+                                                      num_worst_tokens=n_worst, config=cfg)
+                buf.combine(rxb, hb, topk_weights=rtwb, config=cfg)
+                cap_stream.synchronize()
+                if world > 1:
+                    dist.barrier()
+                gd, gc = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gd, stream=cap_stream):
+                    kd = buf.dispatch(x0, num_tokens_per_rank=pr0, is_token_in_rank=ir0, num_tokens_per_expert=pe0,
+                                      topk_idx=idx0, topk_weights=w0, num_worst_tokens=n_worst, config=cfg)
+                with torch.cuda.graph(gc, stream=cap_stream):
+                    kc = buf.combine(rxb, hb, topk_weights=rtwb, config=cfg)
+            torch.cuda.current_stream().wait_stream(cap_stream)
+            barrier()
+            res_ms = {}
+            for name, g_ in (("dispatch", gd), ("combine", gc)):
+                for _ in range(3):
+                    g_.replay()
+                barrier()
+                k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                k0.record()
+                for _ in range(args.steps):
+                    g_.replay()
+                k1.record()
+                barrier()
+                res_ms[name] = max_over_ranks(k0.elapsed_time(k1)) / args.steps
+            rows0 = rows[0]
+            rem0 = max_over_ranks(float(remote_rows[0]))
+            ent = {"dispatch_us": round(res_ms["dispatch"] * 1e3, 2), "combine_us": round(res_ms["combine"] * 1e3, 2)}
+            if R == 1:
+                ent["dispatch_hbm_gbs"] = round(2.0 * rows0 * ROW / (res_ms["dispatch"] / 1e3) / 1e9, 1)
+                ent["combine_hbm_gbs"] = round(2.0 * rows0 * ROW / (res_ms["combine"] / 1e3) / 1e9, 1)
+            else:
+                ent["dispatch_nvlink_gbs"] = round(rem0 * ROW / (res_ms["dispatch"] / 1e3) / 1e9, 1)
+                ent["combine_nvlink_gbs"] = round(rem0 * ROW / (res_ms["combine"] / 1e3) / 1e9, 1)
+            sm_budget[str(n_sms)] = ent
+            del gd, gc, kd, kc, rxb, rtwb, hb
+            barrier()
+    del fixed
 
     # ---- roofline of the dominant kernel -------------------------------------------------
     hbm_peak, peak_kind = _peaks()
@@ -663,9 +735,9 @@ def run_ours(args):
                                "local rows included) / max-over-ranks step time",
                 "per_gpu_gbs": round(value / R, 3),
                 "verified": {"verified": all(v.get("verified") for v in verified.values()), **verified},
-                "step_mode": f"CUDA graph per step (layout -> dispatch(num_worst_tokens={n_worst}) -> combine), "
-                             "replayed back to back",
-                "eager": eager, "kernels_ms": kernels_ms, "nvlink_hw": nvlink, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
+                "step_mode": f"CUDA graphs of {NSETS} consecutive steps (layout -> dispatch(num_worst_tokens="
+                             f"{n_worst}) -> combine per step), replayed back to back",
+                "eager": eager, "kernels_ms": kernels_ms, "sm_budget": sm_budget, "nvlink_hw": nvlink, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_scope": "per rank",
                 "clocks": clocks.summary(), "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)

@@ -440,7 +440,27 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     int n[kMaxRanks];
 #pragma unroll
     for (int d = 0; d < kMaxRanks; ++d) n[d] = 0;
-    for (int t = tid; t < t0; t += blockDim.x) {
+    // 16-byte loads over the [t0, R] bool bytes (R | 16: byte j of a word is
+    // destination j % R): one load round for the whole prefix instead of one
+    // dependent byte-load round per 512 tokens
+    int t_scalar = 0;
+    if (16 % R == 0 && (reinterpret_cast<uintptr_t>(a.is_token_in_rank) & 15) == 0) {
+      const int nw16 = (t0 * R) >> 4;
+      const uint4* ir4 = reinterpret_cast<const uint4*>(a.is_token_in_rank);
+      for (int i = tid; i < nw16; i += blockDim.x) {
+        const uint4 w = ir4[i];
+        const uint32_t q[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t b = (q[j >> 2] >> (8 * (j & 3))) & 0xffu;
+#pragma unroll
+          for (int d = 0; d < kMaxRanks; ++d)
+            if (d < R && j % R == d) n[d] += b != 0;
+        }
+      }
+      t_scalar = (nw16 << 4) / R;
+    }
+    for (int t = t_scalar + tid; t < t0; t += blockDim.x) {
       uint64_t bits = 0;  // the token's R bool bytes (one aligned load for R = 2, 4, 8)
       const uint8_t* row = a.is_token_in_rank + (size_t)t * R;
       if (R == 8) bits = *reinterpret_cast<const uint64_t*>(row);
@@ -517,7 +537,17 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     if (tid == 0) s_before = 0;
     __syncthreads();
     int n = 0;
-    for (int i = tid; i < t0; i += blockDim.x) n += a.is_token_in_rank[i] != 0;
+    int i_scalar = 0;
+    if ((reinterpret_cast<uintptr_t>(a.is_token_in_rank) & 15) == 0) {  // 16 bool bytes per load
+      const uint4* ir4 = reinterpret_cast<const uint4*>(a.is_token_in_rank);
+      for (int i = tid; i < (t0 >> 4); i += blockDim.x) {
+        const uint4 w = ir4[i];
+        n += __popc(w.x & 0x01010101u) + __popc(w.y & 0x01010101u) + __popc(w.z & 0x01010101u) +
+             __popc(w.w & 0x01010101u);
+      }
+      i_scalar = t0 & ~15;
+    }
+    for (int i = i_scalar + tid; i < t0; i += blockDim.x) n += a.is_token_in_rank[i] != 0;
     n = __reduce_add_sync(0xffffffffu, n);
     if (lane == 0 && n) atomicAdd(&s_before, n);
     __syncthreads();
