@@ -721,6 +721,26 @@ def run_ours(args):
         except Exception as exc:  # keep the headline even if a transport is unavailable
             ll[transport] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
+    # ---- GPU -> CPU FIFO: device-producer command rate --
+    fifo = None
+    if not args.no_ll:
+        try:
+            import ctypes as C
+            from paper_2512_19849_b200._lib import check, lib
+            if not buf._rank.proxy_running:
+                check(lib.epb_proxy_start(buf._rank.ctx))
+                buf._rank.proxy_running = True
+            n_cmds, chans = 1 << 20, 8
+            el = C.c_int64()
+            check(lib.epb_fifo_device_bench(buf._rank.ctx, n_cmds, chans, C.byref(el),
+                                            torch.cuda.current_stream().cuda_stream))
+            fifo = {"mcmd_s": round(n_cmds / (el.value / 1e9) / 1e6, 2), "commands": n_cmds, "channels": chans,
+                    "proxy_threads": buf._rank.cfg.proxy_threads,
+                    "how": "one producer warp per channel pushes 16-byte TransferCmds in 32-slot bursts into pinned "
+                           "rings; the proxy threads pop them (count-only) and publish COMPLETED; device-timed "
+                           "until every command is completed"}
+        except Exception as exc:  # noqa: BLE001
+            fifo = {"error": f"{type(exc).__name__}: {exc}"[:200]}
     buf._g.check_device_error()
     line = None
     if rank == 0:
@@ -737,7 +757,8 @@ def run_ours(args):
                 "verified": {"verified": all(v.get("verified") for v in verified.values()), **verified},
                 "step_mode": f"CUDA graphs of {NSETS} consecutive steps (layout -> dispatch(num_worst_tokens="
                              f"{n_worst}) -> combine per step), replayed back to back",
-                "eager": eager, "kernels_ms": kernels_ms, "sm_budget": sm_budget, "nvlink_hw": nvlink, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
+                "eager": eager, "kernels_ms": kernels_ms, "sm_budget": sm_budget, "nvlink_hw": nvlink,
+                "fifo_device_producer": fifo, "roofline": roofline, "e2e": e2e, "ll_us": ll, "configs": configs,
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_scope": "per rank",
                 "clocks": clocks.summary(), "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)

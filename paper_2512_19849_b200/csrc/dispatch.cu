@@ -380,6 +380,43 @@ __device__ __noinline__ void push_dispatch_cmds(const DispatchParams& P, int lr,
   }
 }
 
+// Row metadata of token t: lane j < k holds topk_idx / weight j, lanes hold
+// up to two of the S scales (S <= 64).
+constexpr int kMetaTok = 2;
+__device__ __forceinline__ void meta_load(const epb_dispatch_args_t& a, int t, int lane, int64_t& e, float& w,
+                                          float* sc) {
+  const int k = a.num_topk, S = a.num_scales;
+  e = (a.topk_idx != nullptr && lane < k) ? a.topk_idx[(size_t)t * k + lane] : -1;
+  w = (a.topk_weights != nullptr && lane < k) ? a.topk_weights[(size_t)t * k + lane] : 0.0f;
+  sc[0] = (a.x_scales != nullptr && lane < S) ? a.x_scales[(size_t)t * S + lane] : 0.0f;
+  sc[1] = (a.x_scales != nullptr && lane + 32 < S) ? a.x_scales[(size_t)t * S + lane + 32] : 0.0f;
+}
+__device__ __forceinline__ void meta_store(const DispatchParams& P, int lr, int t, int tt, const int32_t* s_pos,
+                                           char* const* s_dst, const int32_t* s_rb, int64_t e, float w,
+                                           const float* sc, int lane) {
+  const epb_dispatch_args_t& a = P.a[lr];
+  const int R = P.rv[lr].world, k = a.num_topk, S = a.num_scales;
+  const int L = (a.topk_idx != nullptr && a.num_experts > 0) ? a.num_experts / R : 0;
+  for (int d = 0; d < R; ++d) {
+    const int p = s_pos[tt * R + d];
+    if (p < 0) continue;
+    const size_t row = (size_t)(s_rb[d] + p);
+    char* slot = s_dst[d];
+    if (a.x_scales != nullptr) {
+      float* ds = reinterpret_cast<float*>(slot + P.lay.off_scales) + row * S;
+      if (lane < S) ds[lane] = sc[0];
+      if (lane + 32 < S) ds[lane + 32] = sc[1];
+    }
+    if (a.topk_idx != nullptr && lane < k) {
+      const int64_t le = (e >= (int64_t)d * L && e < (int64_t)(d + 1) * L) ? e - (int64_t)d * L : -1;
+      reinterpret_cast<int64_t*>(slot + P.lay.off_topk_idx)[row * k + lane] = le;
+      if (a.topk_weights != nullptr)
+        reinterpret_cast<float*>(slot + P.lay.off_topk_w)[row * k + lane] = le >= 0 ? w : 0.0f;
+    }
+    if (lane == 0) reinterpret_cast<int32_t*>(slot + P.lay.off_src_idx)[row] = t;
+  }
+}
+
 __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __grid_constant__ DispatchParams P) {
   const int lr = blockIdx.y;
   const RankView& rv = P.rv[lr];
@@ -601,14 +638,23 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
     }
     const size_t row_bytes = (size_t)a.hidden * a.elem_bytes;
     const int n16 = (int)(row_bytes >> 4);
-    const int k = a.num_topk, S = a.num_scales;
-    const int L = (a.topk_idx != nullptr && a.num_experts > 0) ? a.num_experts / R : 0;
     // Rows move in units of (token, 3.5 KB segment), two units in flight per
     // warp (14 x 16 B loads per lane): the channel's ~28 tokens x 4 segments
     // spread evenly over the block's warps (whole rows left the slowest warp
     // with 2 rows against a mean of 1.75), and each row is read from HBM once
     // and stored to every destination that needs it.
     const int wc = warp - first_copy_warp, nwc = nwarps - first_copy_warp;
+    // this warp's first kMetaTok tokens: metadata loads issued now, stored after the rows
+    int64_t m_e[kMetaTok];
+    float m_w[kMetaTok], m_sc[kMetaTok][2];
+#pragma unroll
+    for (int q = 0; q < kMetaTok; ++q) {
+      const int tt = wc + q * nwc;
+      m_e[q] = -1;
+      m_w[q] = 0.0f;
+      m_sc[q][0] = m_sc[q][1] = 0.0f;
+      if (!P.notify_only && wc >= 0 && tt < nt) meta_load(a, t0 + tt, lane, m_e[q], m_w[q], m_sc[q]);
+    }
     constexpr int kSeg = 32 * kCopyUnroll;
     const int segs = (n16 + kSeg - 1) / kSeg;
     const int units = P.notify_only ? 0 : nt * segs;
@@ -643,28 +689,19 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
         }
       }
     }
-    // per-row metadata: scales, mapped top-k, source index
-    for (int tt = wc; !P.notify_only && wc >= 0 && tt < nt; tt += nwc) {
-      const int t = t0 + tt;
-      for (int d = 0; d < R; ++d) {
-        const int p = s_pos[tt * R + d];
-        if (p < 0) continue;
-        const size_t row = (size_t)(s_rb[d] + p);
-        char* slot = s_dst[d];
-        if (a.x_scales != nullptr) {
-          float* ds = reinterpret_cast<float*>(slot + P.lay.off_scales) + row * S;
-          for (int i = lane; i < S; i += 32) ds[i] = a.x_scales[(size_t)t * S + i];
-        }
-        if (a.topk_idx != nullptr && lane < k) {
-          const int64_t e = a.topk_idx[(size_t)t * k + lane];
-          const int64_t le = (e >= (int64_t)d * L && e < (int64_t)(d + 1) * L) ? e - (int64_t)d * L : -1;
-          reinterpret_cast<int64_t*>(slot + P.lay.off_topk_idx)[row * k + lane] = le;
-          if (a.topk_weights != nullptr)
-            reinterpret_cast<float*>(slot + P.lay.off_topk_w)[row * k + lane] =
-                le >= 0 ? a.topk_weights[(size_t)t * k + lane] : 0.0f;
-        }
-        if (lane == 0) reinterpret_cast<int32_t*>(slot + P.lay.off_src_idx)[row] = t;
-      }
+    // per-row metadata: scales, mapped top-k, source index.  The values were
+    // loaded before the copy loop (meta_load), so their latency is hidden.
+    for (int q = 0; q < kMetaTok; ++q) {
+      const int tt = wc + q * nwc;
+      if (P.notify_only || wc < 0 || tt >= nt) break;
+      meta_store(P, lr, t0 + tt, tt, s_pos, s_dst, s_rb, m_e[q], m_w[q], m_sc[q], lane);
+    }
+    for (int tt = wc + kMetaTok * nwc; !P.notify_only && wc >= 0 && tt < nt; tt += nwc) {
+      int64_t e;
+      float w;
+      float sc[2];
+      meta_load(a, t0 + tt, lane, e, w, sc);
+      meta_store(P, lr, t0 + tt, tt, s_pos, s_dst, s_rb, e, w, sc, lane);
     }
   }
 
@@ -745,6 +782,8 @@ static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_a
     const epb_dispatch_args_t& a = args[i];
     if (a.elem_bytes != 1 && a.elem_bytes != 2) return epb_set_error(EPB_ERR_CONFIG, "elem_bytes must be 1 or 2");
     if (((size_t)a.hidden * a.elem_bytes) % 16 != 0) return epb_set_error(EPB_ERR_CONFIG, "row bytes must be 16-aligned");
+    if (a.num_scales > 64) return epb_set_error(EPB_ERR_CONFIG, "at most 64 scales per row (hidden <= 8192 with FP8)");
+    if (a.num_topk > 32) return epb_set_error(EPB_ERR_CONFIG, "num_topk must be <= 32");
     if (a.num_experts > 0 &&
         (a.num_experts % ctxs[i]->world != 0 || a.num_experts / ctxs[i]->world > kMaxLocalExperts))
       return epb_set_error(EPB_ERR_CONFIG, "num_experts must be a multiple of world (<= 1024 local experts)");
