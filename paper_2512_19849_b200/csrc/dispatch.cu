@@ -37,7 +37,12 @@
 namespace epb {
 
 constexpr int kDispatchThreads = 512;
-constexpr int kCopyUnroll = 7;  // 7 x 16 B per lane in flight = 3.5 KB per warp
+constexpr int kCopyUnroll = 7;
+// Bulk-copy (TMA) path: kTmaWarps warps per block each drive a ring of
+// kTmaStages units of <= 8 KB through shared memory (global -> shared bulk
+// load with an mbarrier, shared -> global bulk store per destination).
+constexpr int kTmaWarps = 6, kTmaStages = 4, kTmaSegMax = 8192;
+constexpr int kTmaAutoChannels = 48;  // bulk copies by default at <= 48 channels (SM budgets)  // 7 x 16 B per lane in flight = 3.5 KB per warp
 
 // Inclusive/exclusive scan of n <= 32*k ints in shared memory by one warp;
 // writes the inclusive row to `incl_out` and the exclusive row to
@@ -75,6 +80,9 @@ struct DispatchParams {
                                 // exchange (its channel is empty) and every other block derives its own
                                 // channel offset, so copies start without waiting for the plan
   int fifo_channels;
+  int tma;                      // rows move through per-warp shared-memory rings with bulk copies
+  int tma_seg;                  // bytes per bulk unit (a row, or a part of it)
+  int tma_smem_off;             // byte offset of the rings in dynamic shared memory
   uint64_t ht_calls[kMaxLocal];  // proxy transport: expected ht_sig[0][src] (calls so far)
   uint32_t host_seq[kMaxLocal];  // tag of this call's host words (the host's call counter); the
                                  // mailbox epoch and done targets are device-resident (norm_call_begin)
@@ -655,9 +663,63 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
       m_sc[q][0] = m_sc[q][1] = 0.0f;
       if (!P.notify_only && wc >= 0 && tt < nt) meta_load(a, t0 + tt, lane, m_e[q], m_w[q], m_sc[q]);
     }
+    if (P.tma && !P.notify_only) {
+      // Bulk-copy path: warp w < kTmaWarps (of the copy warps), lane 0, runs a
+      // kTmaStages-deep ring: unit i = (token, segment) is bulk-loaded into its
+      // stage (mbarrier), bulk-stored to every destination (one bulk group),
+      // and its stage is refilled with unit i + kTmaStages - 1 once the group of
+      // unit i - 1 has finished reading shared memory.
+      __shared__ __align__(8) uint64_t s_bar[kTmaWarps][kTmaStages];
+      extern __shared__ __align__(128) uint8_t s_dyn[];
+      const int seg = P.tma_seg, nseg = (int)((row_bytes + seg - 1) / seg);
+      const int tma_units = nt * nseg;
+      if (wc >= 0 && wc < kTmaWarps && lane == 0) {
+        uint8_t* ring = s_dyn + P.tma_smem_off + (size_t)wc * kTmaStages * seg;
+        const uint64_t pol = l2_policy_evict_last();
+        uint64_t* bar = s_bar[wc];
+        for (int st = 0; st < kTmaStages; ++st) mbar_init(&bar[st], 1);
+        fence_async_shared();
+        const int n_my = tma_units > wc ? (tma_units - wc + kTmaWarps - 1) / kTmaWarps : 0;
+        auto unit_src = [&](int i, uint32_t& len) -> const char* {
+          const int u = wc + i * kTmaWarps, tt = u / nseg, sg = u % nseg;
+          const size_t off = (size_t)sg * seg;
+          len = (uint32_t)min((size_t)seg, row_bytes - off);
+          return static_cast<const char*>(a.x) + (size_t)(t0 + tt) * row_bytes + off;
+        };
+        auto issue_load = [&](int i) {
+          uint32_t len;
+          const char* src = unit_src(i, len);
+          const int st = i % kTmaStages;
+          mbar_expect_tx(&bar[st], len);
+          bulk_load(ring + (size_t)st * seg, src, len, &bar[st]);
+        };
+        for (int i = 0; i < min(n_my, kTmaStages - 1); ++i) issue_load(i);
+        for (int i = 0; i < n_my; ++i) {
+          const int st = i % kTmaStages;
+          while (!mbar_try_wait(&bar[st], (uint32_t)((i / kTmaStages) & 1))) {
+          }
+          const int u = wc + i * kTmaWarps, tt = u / nseg, sg = u % nseg;
+          const size_t off = (size_t)sg * seg;
+          const uint32_t len = (uint32_t)min((size_t)seg, row_bytes - off);
+          for (int d = 0; d < R; ++d) {
+            const int p = s_pos[tt * R + d];
+            if (p < 0) continue;
+            char* dst = s_dst[d] + P.lay.off_x + (size_t)(s_rb[d] + p) * row_bytes + off;
+            if (P.tma == 2) bulk_store_hint(dst, ring + (size_t)st * seg, len, pol);
+            else bulk_store(dst, ring + (size_t)st * seg, len);
+          }
+          bulk_commit();
+          if (i + kTmaStages - 1 < n_my) {
+            bulk_wait_read<1>();  // unit i - 1's stores have read the stage unit i + S - 1 reuses
+            issue_load(i + kTmaStages - 1);
+          }
+        }
+        bulk_wait_all();
+      }
+    }
     constexpr int kSeg = 32 * kCopyUnroll;
     const int segs = (n16 + kSeg - 1) / kSeg;
-    const int units = P.notify_only ? 0 : nt * segs;
+    const int units = (P.notify_only || P.tma) ? 0 : nt * segs;
     for (int u = wc; wc >= 0 && u < units; u += 2 * nwc) {
       int4 v[2][kCopyUnroll];
 #pragma unroll
@@ -797,8 +859,36 @@ static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_a
       max_tc = std::max(max_tc, (a.num_tokens + num_channels - 2) / (num_channels - 1));
     }
   }
-  const size_t smem = sizeof(int32_t) * (size_t)max_tc * ctxs[0]->world;
+  size_t smem = sizeof(int32_t) * (size_t)max_tc * ctxs[0]->world;
   if (smem > 160 * 1024) return epb_set_error(EPB_ERR_CONFIG, "too many tokens per channel; raise num_sms");
+  // Bulk-copy rows (TMA engine) when the dispatch runs on a small SM budget:
+  // at 20 / 24 / 48 channels it moves the DS-V3 rows 11-13 % faster than the
+  // warp copy; on the whole GPU the warp copy wins the step (the combine behind
+  // a bulk-copied dispatch ran slower: 59 against 52 us per N=1 step,
+  // profiles/r02_summary.md).  EPB_TMA=0 / 1 / 2 forces off / on / on with an
+  // L2 evict_last hint on the bulk stores.
+  static const int tma_env = [] {
+    const char* v = std::getenv("EPB_TMA");
+    return v ? std::atoi(v) : -1;
+  }();
+  const int tma_want = tma_env >= 0 ? tma_env : (num_channels <= kTmaAutoChannels ? 1 : 0);
+  P.tma = 0;
+  if (tma_want && !notify_only) {
+    const size_t rb = (size_t)args[0].hidden * args[0].elem_bytes;
+    const int nseg = (int)((rb + kTmaSegMax - 1) / kTmaSegMax);
+    const int seg = (int)align_up((rb + nseg - 1) / nseg, 16);
+    const size_t off = align_up(smem, 128);
+    const size_t need = off + (size_t)kTmaWarps * kTmaStages * seg;
+    bool ok = need <= 200 * 1024;
+    for (int i = 0; i < n_local && ok; ++i)
+      ok = (reinterpret_cast<uintptr_t>(args[i].x) & 15) == 0 && (size_t)args[i].hidden * args[i].elem_bytes == rb;
+    if (ok) {
+      P.tma = tma_want;  // 2: bulk stores carry an L2 evict_last hint
+      P.tma_seg = seg;
+      P.tma_smem_off = (int)off;
+      smem = need;
+    }
+  }
   // max shared carveout: the N=1 step (layout, dispatch, combine back to back)
   // took 70 us with the driver's choice and 63 us with this, although the
   // dispatch alone is ~2 us slower; the gain is in the gap after the dispatch
