@@ -38,6 +38,8 @@ struct CombineParams {
   int fifo_channels;
   uint64_t ht_calls[kMaxLocal];  // proxy transport: expected ht_sig[1][src]
   int seg16;                     // reduce work unit: 16-byte columns per (token, segment); 0 = whole rows
+  int tma;                       // reduce from shared memory filled by bulk copies (small SM budgets)
+  int tma_seg;                   // bytes per partial per bulk unit
   int bump;                      // this launch ends the call: store the next epoch / done target
                                  // (device-resident, norm_call_begin/_end; the proxy's stage launch does not)
   RankView rv[kMaxLocal];
@@ -138,6 +140,104 @@ __device__ __forceinline__ void zero_row(int4* out, int i0, int n16, int lane) {
 // overlaps the mode exchange / barrier); blocks with more tokens read global
 constexpr int kShTokens = 64;
 
+// Bulk-copy reduce (small SM budgets, where a warp's few 16-byte loads in
+// flight cannot cover NVLink latency): warps [0, kCombTmaWarps) each run a
+// ring of kCombTmaStages stages; a unit = (token, segment) and its stage holds
+// the segment of every contributing partial, bulk-loaded (cp.async.bulk, the
+// TMA engine) from the partial's row — a peer's input over NVLink (pull) or my
+// staging (push) — against one mbarrier.  All 32 lanes then reduce the stage
+// in fp32, ascending rank order (the canonical order, bit-identical to the
+// register path), round once to bf16 and store.
+constexpr int kCombTmaWarps = 4, kCombTmaStages = 3;
+
+__device__ __noinline__ void reduce_tokens_bulk(const CombineParams& P, int lr, const RowSrc& rs,
+                                               const int32_t (*s_sh)[kMaxRanks], int tb0, int tb1, bool cached) {
+  const epb_combine_args_t& a = P.a[lr];
+  const int R = P.rv[lr].world, k = a.num_topk;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t row_bytes = rs.row_bytes;
+  const int seg = P.tma_seg, nseg = (int)((row_bytes + seg - 1) / seg);
+  const int units = (tb1 - tb0) * nseg;
+  __shared__ __align__(8) uint64_t s_bar[kCombTmaWarps][kCombTmaStages];
+  extern __shared__ __align__(128) uint8_t s_ring[];
+  // the block's send_head rows, staged once in shared memory after the rings
+  // (unit bookkeeping must not wait on global loads: lane 0 issues the copies)
+  int32_t* s_shb = reinterpret_cast<int32_t*>(s_ring + (size_t)kCombTmaWarps * kCombTmaStages * R * seg);
+  for (int i = tid; i < (tb1 - tb0) * R; i += blockDim.x) s_shb[i] = a.send_head[(size_t)tb0 * R + i];
+  __syncthreads();
+  if (warp >= kCombTmaWarps) return;
+  uint8_t* ring = s_ring + (size_t)warp * kCombTmaStages * R * seg;
+  uint64_t* bar = s_bar[warp];
+  if (lane == 0) {
+    for (int st = 0; st < kCombTmaStages; ++st) mbar_init(&bar[st], 1);
+    fence_async_shared();
+  }
+  __syncwarp();
+  const int n_my = units > warp ? (units - warp + kCombTmaWarps - 1) / kCombTmaWarps : 0;
+  auto unit_info = [&](int i, int& t, size_t& off, uint32_t& len, const int32_t*& sh, uint32_t& mask) {
+    const int u = warp + i * kCombTmaWarps;
+    t = tb0 + u / nseg;
+    off = (size_t)(u % nseg) * seg;
+    len = (uint32_t)min((size_t)seg, row_bytes - off);
+    sh = s_shb + (size_t)(t - tb0) * R;
+    mask = 0;
+    for (int d = 0; d < R; ++d)
+      if (sh[d] >= 0) mask |= 1u << d;
+  };
+  auto issue = [&](int i) {  // lane 0
+    int t;
+    size_t off;
+    uint32_t len, mask;
+    const int32_t* sh;
+    unit_info(i, t, off, len, sh, mask);
+    const int st = i % kCombTmaStages;
+    mbar_expect_tx(&bar[st], len * (uint32_t)__popc(mask));
+    int j = 0;
+    for (uint32_t m = mask; m != 0; m &= m - 1, ++j) {
+      const int d = __ffs(m) - 1;
+      const char* src = rs.base[d] + (size_t)(rs.row0[d] + sh[d]) * row_bytes + off;
+      bulk_load(ring + ((size_t)st * R + j) * seg, src, len, &bar[st]);
+    }
+  };
+  if (lane == 0)
+    for (int i = 0; i < min(n_my, kCombTmaStages); ++i) issue(i);
+  for (int i = 0; i < n_my; ++i) {
+    const int st = i % kCombTmaStages;
+    int t;
+    size_t off;
+    uint32_t len, mask;
+    const int32_t* sh;
+    unit_info(i, t, off, len, sh, mask);
+    while (!mbar_try_wait(&bar[st], (uint32_t)((i / kCombTmaStages) & 1))) {
+    }
+    const int nv = __popc(mask);
+    const int4* stage = reinterpret_cast<const int4*>(ring + (size_t)st * R * seg);
+    int4* out = reinterpret_cast<int4*>(static_cast<char*>(a.combined_x) + (size_t)t * row_bytes + off);
+    const int n16 = (int)(len >> 4), s16 = seg >> 4;
+    for (int c = lane; c < n16; c += 32) {
+      float acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+      for (int j = 0; j < nv; ++j) acc_bf16x8(acc, stage[(size_t)j * s16 + c]);
+      st_na_v4(out + c, pack_bf16x8(acc));
+    }
+    if (off == 0 && a.combined_topk_weights != nullptr && lane < k) {
+      float w = 0.0f;
+      for (uint32_t m = mask; m != 0; m &= m - 1) {
+        const int d = __ffs(m) - 1;
+        const float* wsrc = reinterpret_cast<const float*>(rs.wbase[d]);
+        if (wsrc != nullptr) w = __fadd_rn(w, wsrc[(size_t)(rs.row0[d] + sh[d]) * k + lane]);
+      }
+      a.combined_topk_weights[(size_t)t * k + lane] = w;
+    }
+    __syncwarp();  // every lane has read the stage
+    if (lane == 0 && i + kCombTmaStages < n_my) {
+      fence_async_shared();  // generic-proxy reads of the stage before its async-proxy refill
+      issue(i + kCombTmaStages);
+    }
+  }
+}
+
 template <int kMaxFan>
 __device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bool pull, const int64_t* s_xoff,
                                               const int64_t* s_woff, const int32_t* s_excl, const int32_t* s_mypre,
@@ -173,6 +273,10 @@ __device__ __forceinline__ void reduce_tokens(const CombineParams& P, int lr, bo
   }
   __syncthreads();
   const bool cached = tb1 - tb0 <= kShTokens;
+  if (P.tma) {
+    reduce_tokens_bulk(P, lr, rs, s_sh, tb0, tb1, cached);
+    return;
+  }
   const int seg16 = P.seg16 > 0 ? P.seg16 : n16;
   const int segs = (n16 + seg16 - 1) / seg16;
   for (int unit = warp; unit < (tb1 - tb0) * segs; unit += nwarps) {
@@ -490,13 +594,8 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
   int nb = std::max(1, num_sms / n_local);
   // one rank (EP=1): every token has fan-in 1 -> the 12-warp copy instantiation
   const bool solo = ctxs[0]->world == 1;
-  static const bool wide = [] {  // measurement knob: 12-warp multi-rank instantiation (register-capped)
-    const char* v = std::getenv("EPB_COMBINE_WIDE");
-    return v && v[0] == '1';
-  }();
-  const void* kern = solo ? (const void*)combine_kernel<1, kCombineThreadsSolo>
-                     : wide ? (const void*)combine_kernel<8, 384> : (const void*)combine_kernel<8, kCombineThreads>;
-  const int threads = solo ? kCombineThreadsSolo : wide ? 384 : kCombineThreads;
+  const void* kern = solo ? (const void*)combine_kernel<1, kCombineThreadsSolo> : (const void*)combine_kernel<8, kCombineThreads>;
+  const int threads = solo ? kCombineThreadsSolo : kCombineThreads;
   // reduce work unit: whole rows (3.5 KB row segments measured slower: EP=2 135
   // against 124 us, EP=1 22.6 against 21.8 us per combine; profiles/r02_summary.md).
   // EPB_COMBINE_SEG16 = 16-byte columns per segment (measurement knob).
@@ -505,7 +604,35 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     return v ? std::atoi(v) : -1;
   }();
   P.seg16 = seg_env >= 0 ? seg_env : 0;
-  const int max_active = epb_max_active_blocks(kern, threads, 0);
+  // bulk-copy reduce: opt-in only (EPB_TMA=1).  Parity-green, but measured slower
+  // than the register path at every SM budget (N=1, 20/24/48 SMs: 280/239/124 us
+  // against 76/66/38 us; profiles/r02_tma_ab_n1.txt): 4 warps x 3 stages of
+  // segments in flight per block cannot match 16 warps of 16-byte loads.
+  static const int tma_env = [] {
+    const char* v = std::getenv("EPB_TMA");
+    return v ? std::atoi(v) : -1;
+  }();
+  size_t smem = 0;
+  if (tma_env > 0 && !P.proxy) {
+    const int R = ctxs[0]->world;
+    const size_t rb = (size_t)args[0].hidden * 2;
+    int seg = (int)std::min<size_t>(8192, 16384 / (size_t)R) & ~15;
+    seg = (int)std::min<size_t>((size_t)seg, rb);
+    int tmax = 0;
+    for (int i = 0; i < n_local; ++i) tmax = std::max(tmax, args[i].num_tokens);
+    // rings + the send_head cache of a block's tokens (nb only shrinks below, by
+    // co-residency, which 1 block/SM with <= 200 KB keeps)
+    const size_t need = (size_t)kCombTmaWarps * kCombTmaStages * R * seg + (size_t)((tmax + nb - 1) / nb) * R * 4;
+    bool ok = (rb % 16) == 0 && need <= 200 * 1024 && nb <= ctxs[0]->num_sms / n_local;
+    for (int i = 0; i < n_local && ok; ++i) ok = (size_t)args[i].hidden * 2 == rb;
+    if (ok) {
+      P.tma = 1;
+      P.tma_seg = seg;
+      smem = need;
+      EPB_CUDA(epb_ensure_smem(kern, smem));
+    }
+  }
+  const int max_active = epb_max_active_blocks(kern, threads, smem);
   nb = std::min(nb, std::max(1, max_active * ctxs[0]->num_sms / n_local));
   for (int i = 0; i < n_local; ++i) {
     epb_ctx* c = ctxs[i];
@@ -530,7 +657,7 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     return EPB_OK;
   }
   P.bump = 1;
-  EPB_CUDA(epb_launch_grid_sync(kern, dim3(nb, n_local), dim3(threads), kargs, 0, st));
+  EPB_CUDA(epb_launch_grid_sync(kern, dim3(nb, n_local), dim3(threads), kargs, smem, st));
   return EPB_OK;
 }
 

@@ -96,9 +96,11 @@ struct Scratch {                         // private to the owning rank
   // can be captured in CUDA graphs and replayed: [dispatch|combine]
   uint32_t ll_epoch[2];
   uint32_t ll_pcnt[2];                   // proxy-transport calls so far (signal targets)
-  // LL proxy transport: arrivals per command group [dispatch|combine][group];
-  // the warp whose arrival completes a group pushes its WRITE and resets it
-  uint32_t llp_grp[2][kMaxFifo];
+  // LL proxy transport: arrivals per command group [dispatch|combine][parity][group];
+  // the add that completes a group pushes its WRITE; the call's last block
+  // (ticket) zeroes its parity's counters, so a call that aborted half-way
+  // cannot leave stale arrivals for the calls after it
+  uint32_t llp_grp[2][2][kMaxFifo];
   // LL proxy transport, rows to myself: stored straight into my receive block
   // (no loopback through the proxy); += 1 per completed group [dispatch|combine]
   uint32_t llp_self[2];

@@ -280,14 +280,15 @@ extern "C" int epb_clock_calibrate(int64_t* offset_ns, int64_t* error_ns) {
 extern "C" int64_t epb_debug_ht_sig_offset(void) { return (int64_t)offsetof(epb::Meta, ht_sig); }
 
 // Diagnostics: the LL proxy transport's device-side state, 16 int64:
-// llp_self[2], ll_pcnt[2], ll_epoch[2], llp_grp[0][0..4], llp_grp[1][0..4]
+// llp_self[2], ll_pcnt[2], ll_epoch[2], llp_grp[0][0][0..4], llp_grp[1][0][0..4]
 extern "C" int epb_debug_ll_state(epb_t* ctx, int64_t* out16) {
   if (!ctx || !out16) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
   epb::Scratch sc;
   EPB_CUDA(cudaMemcpy(&sc, epb::scratch_of(ctx->base), sizeof(sc), cudaMemcpyDeviceToHost));
   const int64_t v[16] = {sc.llp_self[0], sc.llp_self[1], sc.ll_pcnt[0], sc.ll_pcnt[1], sc.ll_epoch[0], sc.ll_epoch[1],
-                         sc.llp_grp[0][0], sc.llp_grp[0][1], sc.llp_grp[0][2], sc.llp_grp[0][3], sc.llp_grp[0][4],
-                         sc.llp_grp[1][0], sc.llp_grp[1][1], sc.llp_grp[1][2], sc.llp_grp[1][3], sc.llp_grp[1][4]};
+                         sc.llp_grp[0][0][0], sc.llp_grp[0][0][1], sc.llp_grp[0][0][2], sc.llp_grp[0][0][3],
+                         sc.llp_grp[0][0][4], sc.llp_grp[1][0][0], sc.llp_grp[1][0][1], sc.llp_grp[1][0][2],
+                         sc.llp_grp[1][0][3], sc.llp_grp[1][0][4]};
   std::memcpy(out16, v, sizeof(v));
   return EPB_OK;
 }

@@ -175,7 +175,6 @@ __device__ __noinline__ void ll_push_dispatch_group(const LLDispatchParams& P, i
   const int R = g.R, L = g.L, me = rv.rank, par = epoch & 1;
   const int d = gid % R, c = gid / R;
   Scratch* sc = scratch_of(rv.base);
-  sc->llp_grp[0][gid] = 0;  // complete: no other arrival this call
   char* my_ll = rv.base + P.ll_off;
   if (d == me) {  // my own rows are already in my receive block: header, then count the group
     if (c == 0) {
@@ -407,7 +406,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       __syncthreads();
       for (int gg = tid; gg < G; gg += blockDim.x) {
         const uint32_t n = s_arr[gg];
-        if (n && atom_add_acq_rel_gpu(&sc->llp_grp[0][gg], n) + n == (uint32_t)s_gexp[gg])
+        if (n && atom_add_acq_rel_gpu(&sc->llp_grp[0][par][gg], n) + n == (uint32_t)s_gexp[gg])
           ll_push_dispatch_group(P, lr, gg, s_g0, s_g1, cnt, epoch);
       }
       // off the critical path: the send-block reuse rule held (one PCIe read)
@@ -438,6 +437,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     __syncthreads();
     trace_mark(rv, 27);
     if (s_last && warp == 0) {
+      for (int gg = lane; gg < kMaxFifo; gg += 32) sc->llp_grp[0][par][gg] = 0;
       if (lane == 0) {
         sc->ll_ticket[par] = 0;
         sc->ll_epoch[0] = epoch;
@@ -565,7 +565,6 @@ __device__ __noinline__ void ll_push_combine_group(const LLCombineParams& P, int
   const int R = g.R, me = rv.rank, par = epoch & 1, ch = P.disp_channels + gid;
   const int s = gid % R;
   Scratch* sc = scratch_of(rv.base);
-  sc->llp_grp[1][gid] = 0;
   if (s == me) {  // rows returned to myself were stored into my receive block directly
     red_release_gpu_add(&sc->llp_self[1], 1u);
     return;
@@ -660,7 +659,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
       __syncthreads();
       for (int gg = tid; gg < G; gg += blockDim.x) {
         const uint32_t n = s_arr[gg];
-        if (n && atom_add_acq_rel_gpu(&sc->llp_grp[1][gg], n) + n == (uint32_t)(s_g1[gg] - s_g0[gg]))
+        if (n && atom_add_acq_rel_gpu(&sc->llp_grp[1][par][gg], n) + n == (uint32_t)(s_g1[gg] - s_g0[gg]))
           ll_push_combine_group(P, lr, gg, s_g0, s_g1, epoch);
       }
       if (blockIdx.x == gridDim.x - 1 && tid >= 32 && tid - 32 < G) check_channel_backlog(rv, P.disp_channels + tid - 32, 2);
@@ -672,6 +671,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
     if (tid == 0) s_last = atom_add_acq_rel_gpu(&sc->ll_ticket[2 + par], 1u) == gridDim.x - 1;
     __syncthreads();
     if (s_last && warp == 0) {
+      for (int gg = lane; gg < kMaxFifo; gg += 32) sc->llp_grp[1][par][gg] = 0;
       if (lane == 0) {
         sc->ll_ticket[2 + par] = 0;
         sc->ll_epoch[1] = epoch;
