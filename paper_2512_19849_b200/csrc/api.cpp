@@ -123,6 +123,24 @@ extern "C" int epb_num_sms(void) {
 int epb_fifo_init(epb_ctx* ctx);     // proxy.cpp
 void epb_fifo_free(epb_ctx* ctx);    // proxy.cpp
 
+// Load every kernel of the library into the current device's context up front.
+// With lazy module loading (the CUDA 12 default) a kernel is loaded at its first
+// launch, and that load can wait for the device: an LL call whose dispatch is
+// already spinning on proxy copies while the host issues the first combine
+// launch stalls the proxy threads' copies behind the load (observed: every
+// first LL proxy call of a fresh 4-GPU job timed out).
+static cudaError_t epb_preload_kernels(int device) {
+  static std::mutex m;
+  static bool done[64] = {};
+  std::lock_guard<std::mutex> g(m);
+  if (device < 0 || device >= 64 || done[device]) return cudaSuccess;
+  for (auto fn : {epb_preload_ll, epb_preload_combine, epb_preload_dispatch, epb_preload_layout, epb_preload_chunked,
+                  epb_preload_fifo})
+    if (cudaError_t e = fn()) return e;
+  done[device] = true;
+  return cudaSuccess;
+}
+
 extern "C" int epb_create(epb_t** out, int rank, int world, const epb_config_t* cfg) {
   if (!out || !cfg) return epb_set_error(EPB_ERR_PROTOCOL, "null argument");
   *out = nullptr;
@@ -141,6 +159,7 @@ extern "C" int epb_create(epb_t** out, int rank, int world, const epb_config_t* 
   if (const char* s = std::getenv("EPB_TRACE")) ctx->trace = std::atoi(s) != 0;
   cudaError_t e = cudaGetDevice(&ctx->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  if (e == cudaSuccess) e = epb_preload_kernels(ctx->device);
   ctx->region_bytes = epb::kRegionHeader + epb::align_up(cfg->nvl_bytes, 4096) + epb::align_up(cfg->ll_bytes, 4096);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->base, ctx->region_bytes);
   if (e == cudaSuccess) e = cudaMemset(ctx->base, 0, ctx->region_bytes);

@@ -541,3 +541,11 @@ extern "C" int epb_ring_combine(epb_t* const* ctxs, int n_local, const epb_ring_
                                 0, st));
   return EPB_OK;
 }
+
+// Load this file's kernels now (see epb_preload_kernels, api.cpp).
+cudaError_t epb_preload_chunked() {
+  cudaFuncAttributes attr;
+  for (const void* fn : {(const void*)ring_dispatch_kernel, (const void*)ring_combine_kernel})
+    if (cudaError_t e = cudaFuncGetAttributes(&attr, fn)) return e;
+  return cudaSuccess;
+}

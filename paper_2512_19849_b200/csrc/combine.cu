@@ -661,3 +661,10 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
   return EPB_OK;
 }
 
+// Load this file's kernels now (see epb_preload_kernels, api.cpp).
+cudaError_t epb_preload_combine() {
+  cudaFuncAttributes attr;
+  for (const void* fn : {(const void*)combine_proxy_wait_kernel, (const void*)combine_kernel<1, kCombineThreadsSolo>, (const void*)combine_kernel<8, kCombineThreads>})
+    if (cudaError_t e = cudaFuncGetAttributes(&attr, fn)) return e;
+  return cudaSuccess;
+}

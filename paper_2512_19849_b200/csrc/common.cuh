@@ -104,6 +104,9 @@ struct Scratch {                         // private to the owning rank
   // LL proxy transport, rows to myself: stored straight into my receive block
   // (no loopback through the proxy); += 1 per completed group [dispatch|combine]
   uint32_t llp_self[2];
+  // LL proxy transport, leader polling (EPB_LL_POLL_LEADER): block 0 waits for
+  // the proxies' signals and publishes the call count here for the other blocks
+  uint32_t llp_go[2];
   // normal-mode call epochs and cumulative done targets [dispatch|combine],
   // device-resident so a layout -> dispatch -> combine step can be captured in
   // a CUDA graph and replayed: each call reads them at kernel start and its
@@ -319,6 +322,15 @@ __device__ __forceinline__ void trace_mark_max(const RankView& rv, int idx) {
   }
 }
 
+// Latest time any thread passed this point (the calling thread only).
+__device__ __forceinline__ void trace_mark_max_any(const RankView& rv, int idx) {
+  if (rv.trace) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(reinterpret_cast<unsigned long long*>(&scratch_of(rv.base)->trace[idx]), (unsigned long long)t);
+  }
+}
+
 // gpu-scope acq_rel fetch-add (the last-arriver ticket pattern: each arriving
 // warp releases its prior stores, the winner acquires all of them and its own
 // sys-scope release then covers them by cumulativity).
@@ -430,10 +442,12 @@ __device__ __forceinline__ uint32_t wait_tagged(const RankView& rv, const uint64
   }
 }
 // Same as wait_geq, for a counter written only by this GPU (gpu-scope acquire).
-__device__ __forceinline__ bool wait_geq_gpu(const RankView& rv, const uint32_t* p, uint32_t target, int64_t tag) {
+__device__ __forceinline__ bool wait_geq_gpu(const RankView& rv, const uint32_t* p, uint32_t target, int64_t tag,
+                                             unsigned sleep_ns = 0) {
   uint64_t t0 = 0;
   int iter = 0;
   while (static_cast<int32_t>(ld_acquire_gpu(p) - target) < 0) {
+    if (sleep_ns) __nanosleep(sleep_ns);
     if ((++iter & 1023) == 0) {
       uint64_t now = globaltimer();
       if (t0 == 0) t0 = now;

@@ -65,6 +65,14 @@ cudaError_t epb_ensure_smem(const void* func, size_t smem);
 void epb_set_carveout(const void* func, bool enable = true);
 bool epb_carveout_skip(const char* name);
 
+// Per-file kernel preloads (each .cu), run once per device by epb_create.
+cudaError_t epb_preload_ll();
+cudaError_t epb_preload_combine();
+cudaError_t epb_preload_dispatch();
+cudaError_t epb_preload_layout();
+cudaError_t epb_preload_chunked();
+cudaError_t epb_preload_fifo();
+
 // proxy threads a context runs (proxy.cpp): channel c is served by thread c % n
 int epb_proxy_nthreads(const epb_ctx* ctx);
 

@@ -974,3 +974,11 @@ extern "C" int epb_wait_notify(epb_t* ctx, int64_t* num_recv, int32_t* num_recv_
   }
   return EPB_OK;
 }
+
+// Load this file's kernels now (see epb_preload_kernels, api.cpp).
+cudaError_t epb_preload_dispatch() {
+  cudaFuncAttributes attr;
+  for (const void* fn : {(const void*)dispatch_kernel, (const void*)dispatch_proxy_wait_kernel})
+    if (cudaError_t e = cudaFuncGetAttributes(&attr, fn)) return e;
+  return cudaSuccess;
+}

@@ -306,3 +306,11 @@ extern "C" int epb_get_dispatch_layout(const int64_t* topk_idx, int num_tokens, 
   EPB_CUDA(cudaGetLastError());
   return EPB_OK;
 }
+
+// Load this file's kernels now (see epb_preload_kernels, api.cpp).
+cudaError_t epb_preload_layout() {
+  cudaFuncAttributes attr;
+  for (const void* fn : {(const void*)layout_kernel, (const void*)layout_cluster_kernel})
+    if (cudaError_t e = cudaFuncGetAttributes(&attr, fn)) return e;
+  return cudaSuccess;
+}

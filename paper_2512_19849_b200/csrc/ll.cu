@@ -122,7 +122,7 @@ __device__ __forceinline__ int proxy_cmds_per_call(int G, int R, int me, int cha
 // (my own rows never go through the proxy: they were stored locally and
 // counted on Scratch::llp_self — one add per group, G / R groups per call)
 __device__ __forceinline__ void wait_proxy_groups(const RankView& rv, const Meta* my, int kind, int G, int half, int R,
-                                                  int me, int nth, uint64_t calls, int64_t tag) {
+                                                  int me, int nth, uint64_t calls, int64_t tag, unsigned poll_ns) {
   for (int i = threadIdx.x; i < R * nth; i += blockDim.x) {
     const int s = i / nth, pt = i % nth;
     if (s == me) {
@@ -131,7 +131,27 @@ __device__ __forceinline__ void wait_proxy_groups(const RankView& rv, const Meta
       continue;
     }
     const int n = proxy_cmds_per_call(G, R, me, kind ? half : 0, nth, pt);
-    if (n > 0) wait_geq64(rv, &my->proxy_sig[kind * 32 + pt][s], calls * (uint64_t)n, tag + i, 200);
+    if (n > 0) wait_geq64(rv, &my->proxy_sig[kind * 32 + pt][s], calls * (uint64_t)n, tag + i, poll_ns);
+  }
+}
+
+// The receive wait of the proxy transport.  Default: every block polls the
+// signal words.  leader: block 0 alone polls them (fewer pollers on the lines
+// the copy engines write) and releases the call count to the other blocks.
+// The caller synchronises the block afterwards.
+__device__ __forceinline__ void wait_proxy_recv(const RankView& rv, const Meta* my, int kind, int G, int half, int R,
+                                                int me, int nth, uint64_t calls, int64_t tag, int poll_ns, int leader) {
+  if (!leader) {
+    wait_proxy_groups(rv, my, kind, G, half, R, me, nth, calls, tag, (unsigned)poll_ns);
+    return;
+  }
+  Scratch* sc = scratch_of(rv.base);
+  if (blockIdx.x == 0) {
+    wait_proxy_groups(rv, my, kind, G, half, R, me, nth, calls, tag, (unsigned)poll_ns);
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_gpu(&sc->llp_go[kind], (uint32_t)calls);
+  } else if (threadIdx.x == 0) {
+    wait_geq_gpu(rv, &sc->llp_go[kind], (uint32_t)calls, tag + 0x3f, (unsigned)poll_ns);
   }
 }
 
@@ -141,6 +161,7 @@ __device__ __forceinline__ void wait_proxy_groups(const RankView& rv, const Meta
 struct LLDispatchParams {
   int n_local, phases, use_proxy, disp_channels, pthreads;
   int ngroups;  // proxy transport: command groups (R x groups per destination, <= disp_channels)
+  int poll_ns, poll_leader;  // proxy transport receive polling (ll_poll)
   RankView rv[kMaxLocal];
   epb_ll_dispatch_args_t a[kMaxLocal];
   LLGeom g;
@@ -165,31 +186,25 @@ __device__ __forceinline__ void check_channel_backlog(const RankView& rv, int ch
     report_error(rv, EPB_ERR_PROTOCOL, ((int64_t)0x540 << 32) | ch);
 }
 
-// The single lane whose arrival completed dispatch group gid: the chunk-0
-// group also carries d's per-expert count header; then one WRITE with a
-// piggybacked signal on FIFO channel gid (command.py layout, arena offsets).
+// The single lane whose arrival completed dispatch group gid: one WRITE (the
+// chunk-0 group from the block start: d's per-expert count header, written by
+// block 0, whose arrival the group also awaits) with a piggybacked signal on
+// FIFO channel gid (command.py layout, arena offsets).
 __device__ __noinline__ void ll_push_dispatch_group(const LLDispatchParams& P, int lr, int gid, const int32_t* s_g0,
-                                                    const int32_t* s_g1, const int32_t* cnt, uint32_t epoch) {
+                                                    const int32_t* s_g1, uint32_t epoch) {
   const RankView& rv = P.rv[lr];
   const LLGeom& g = P.g;
-  const int R = g.R, L = g.L, me = rv.rank, par = epoch & 1;
+  const int R = g.R, me = rv.rank, par = epoch & 1;
   const int d = gid % R, c = gid / R;
   Scratch* sc = scratch_of(rv.base);
-  char* my_ll = rv.base + P.ll_off;
-  if (d == me) {  // my own rows are already in my receive block: header, then count the group
-    if (c == 0) {
-      int32_t* h = reinterpret_cast<int32_t*>(my_ll + g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block);
-      for (int le = 0; le < L; ++le) h[le] = cnt[d * L + le];
-    }
+  if (d == me) {  // my own rows (and header) are already in my receive block: count the group
     red_release_gpu_add(&sc->llp_self[0], 1u);
     return;
   }
   const int64_t send_blk = g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
-  if (c == 0) {
-    int32_t* h = reinterpret_cast<int32_t*>(my_ll + send_blk);
-    for (int le = 0; le < L; ++le) h[le] = cnt[d * L + le];
-  }
-  fence_sys();  // the group's rows (acquired through the arrival counter) and the header, before the command
+  // no fence here: fifo_push's st.release.sys of TAIL is cumulative — it orders
+  // the group's rows and header (acquired through the arrival counter) before
+  // the command at system scope (a separate fence.sys cost 2.3 us)
   const int64_t rel = P.ll_off - (int64_t)kRegionHeader;  // commands address the arena start
   const int64_t first = c == 0 ? 0 : g.hdr_bytes + (int64_t)s_g0[gid] * g.disp_row;
   const int64_t len = (c == 0 ? g.hdr_bytes : 0) + (int64_t)(s_g1[gid] - s_g0[gid]) * g.disp_row;
@@ -223,6 +238,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
   const int meta_off = g.use_fp8 ? H + 4 * S : 2 * H;
   extern __shared__ uint8_t smem[];
   trace_mark(rv, 24);
+  trace_mark_max(rv, 39);  // the last block to start
 
   if (sending) {
     const int W = max(1, (T + 31) / 32);
@@ -240,6 +256,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       if (ok) atomicOr(&bm[(size_t)e * W + (t >> 5)], 1u << (t & 31));
     }
     __syncthreads();
+    trace_mark(rv, 30);
     for (int e = tid; e < E; e += blockDim.x) {
       int c = 0;
       for (int w = 0; w < W; ++w) c += __popc(bm[(size_t)e * W + w]);
@@ -247,6 +264,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       pre[e] = c;
     }
     __syncthreads();
+    trace_mark(rv, 62);
     for (int d = warp; d < R; d += nw) warp_scan_smem(pre + d * L, L, lane, true);  // row of expert in dst block
     // proxy transport: token-major rows per destination (a contiguous token
     // range is a contiguous row range, so command groups are row ranges)
@@ -257,62 +275,69 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
     const int G = P.ngroups;
     for (int gg = tid; gg < G; gg += blockDim.x) s_arr[gg] = 0;
     if (P.use_proxy) {
-      for (int t = tid; t < T; t += blockDim.x) {
-        int u[kMaxRanks];
-#pragma unroll
-        for (int d = 0; d < kMaxRanks; ++d) u[d] = 0;
-        for (int j = 0; j < k; ++j) {
-          const int e = s_e[t * k + j];
-          int loc = -1;
-          if (e >= 0) {
-            int first = j;
-            for (int j2 = 0; j2 < j; ++j2)
-              if (s_e[t * k + j2] == e) {
-                first = j2;
-                break;
-              }
-            if (first == j) {
-              const int d = e / L;
-#pragma unroll
-              for (int dd = 0; dd < kMaxRanks; ++dd)
-                if (dd == d) loc = u[dd]++;
-            } else {
-              loc = -2 - first;
-            }
-          }
-          s_loc[t * k + j] = (int16_t)loc;
-        }
-        for (int d = 0; d < R; ++d) rs[d * (T + 1) + t] = u[d];
-      }
-      for (int d = tid; d < R; d += blockDim.x) rs[d * (T + 1) + T] = 0;
+      // per (token, top-k entry): its slot among the token's rows for the entry's
+      // destination (rows = distinct experts, in top-k order), or -2 - j of the
+      // entry j it duplicates.  One lane per entry, kp lanes per token; the
+      // token's other entries come by shuffles (__match_any_sync measured
+      // ~600 cycles per call here)
+      for (int i = tid; i < R * (T + 1); i += blockDim.x) rs[i] = 0;
       __syncthreads();
+      trace_mark(rv, 63);
+      const int kp = k <= 1 ? 1 : 1 << (32 - __clz(k - 1));  // entries rounded to a power of two
+      const int sub = lane / kp, j = lane % kp, l0 = sub * kp;
+      for (int t0 = warp * (32 / kp); t0 < T; t0 += nw * (32 / kp)) {
+        const int t = t0 + sub;
+        const bool entry = t < T && j < k;
+        const int e = entry ? s_e[t * k + j] : -1;
+        int fl = j;  // the token's first entry holding e
+        for (int jj = 0; jj < kp; ++jj) {
+          const int ej = __shfl_sync(0xffffffffu, e, l0 + jj);
+          if (fl == j && jj < j && ej == e) fl = jj;
+        }
+        const bool first = e >= 0 && fl == j;
+        const int dd = first ? e / L : -1;
+        int before = 0, tot = 0;  // first entries of the token for dd: before mine, all
+        for (int jj = 0; jj < kp; ++jj) {
+          const int dj = __shfl_sync(0xffffffffu, dd, l0 + jj);
+          if (first && dj == dd) {
+            ++tot;
+            before += jj < j;
+          }
+        }
+        if (first && before == 0) rs[dd * (T + 1) + t] = tot;
+        if (entry) s_loc[t * k + j] = (int16_t)(first ? before : e < 0 ? -1 : -2 - fl);
+      }
+      __syncthreads();
+      trace_mark(rv, 31);
       for (int d = warp; d < R; d += nw) warp_scan_smem(rs + d * (T + 1), T + 1, lane, true);
       __syncthreads();
       const int NCHc = (H + kChunkCh - 1) / kChunkCh;
-      for (int g = tid; g < G; g += blockDim.x) {
-        const int d = g % R, c = g / R, nc = group_chunks(G, R, d);
+      for (int gi = tid; gi < G; gi += blockDim.x) {
+        const int d = gi % R, c = gi / R, nc = group_chunks(G, R, d);
         const int n = rs[d * (T + 1) + T];
-        s_g0[g] = (int)((int64_t)c * n / nc);
-        s_g1[g] = (int)((int64_t)(c + 1) * n / nc);
-        s_gexp[g] = 0;
+        s_g0[gi] = (int)((int64_t)c * n / nc);
+        s_g1[gi] = (int)((int64_t)(c + 1) * n / nc);
+        // arrivals the group expects: each of its rows, once per chunk item,
+        // and for chunk 0 block 0's header
+        s_gexp[gi] = (s_g1[gi] - s_g0[gi]) * NCHc + (c == 0 ? 1 : 0);
       }
-      __syncthreads();
-      // arrivals a group expects: every item (t, chunk) of each token with a
-      // row in the group arrives once
-      for (int i = tid; i < T * R; i += blockDim.x) {
-        const int t = i / R, d = i % R;
-        const int r_a = rs[d * (T + 1) + t], r_b = rs[d * (T + 1) + t + 1];
-        if (r_b > r_a) {
-          const int g1 = group_of_row(s_g1, G, R, d, r_a), g2 = group_of_row(s_g1, G, R, d, r_b - 1);
-          for (int gg = g1; gg <= g2; gg += R) atomicAdd(&s_gexp[gg], NCHc);
+      if (blockIdx.x == 0) {
+        // block 0 writes every destination's per-expert count header (all
+        // threads; my own into my receive block) and reports it with its rows
+        for (int i = tid; i < R * L; i += blockDim.x) {
+          const int d = i / L;
+          const int64_t blk = d == me ? g.off_disp_recv + (int64_t)(par * R + me) * g.disp_block
+                                      : g.off_disp_send + (int64_t)(par * R + d) * g.disp_block;
+          reinterpret_cast<int32_t*>(my_ll + blk)[i % L] = cnt[i];
         }
+        for (int gg = tid; gg < R && gg < G; gg += blockDim.x) s_arr[gg] = 1;
       }
       __syncthreads();
-      // empty groups (no rows) still send their WRITE (the header for chunk 0):
-      // every group signals once per call
+      // empty groups (no rows, not chunk 0) still send their WRITE: every group
+      // signals once per call
       if (blockIdx.x == 0)
-        for (int g = tid; g < G; g += blockDim.x)
-          if (s_gexp[g] == 0) ll_push_dispatch_group(P, lr, g, s_g0, s_g1, cnt, epoch);
+        for (int gi = tid; gi < G; gi += blockDim.x)
+          if (s_gexp[gi] == 0) ll_push_dispatch_group(P, lr, gi, s_g0, s_g1, epoch);
     }
     __syncthreads();
     trace_mark(rv, 25);
@@ -391,11 +416,11 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
           meta[2] = ordinal_of(bm + (size_t)e * W, t);
         }
       }
-      if (P.use_proxy) {  // count this item once at each group it wrote to (block-local)
+      if (P.use_proxy) {  // count this item's rows at their groups (block-local)
         const unsigned act = __ballot_sync(0xffffffffu, gid >= 0);
         if (gid >= 0) {
           const unsigned peers = __match_any_sync(act, gid);
-          if (lane == __ffs(peers) - 1) atomicAdd(&s_arr[gid], 1u);
+          if (lane == __ffs(peers) - 1) atomicAdd(&s_arr[gid], (uint32_t)__popc(peers));
         }
       }
     }
@@ -404,10 +429,11 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       // one gpu-scope acq_rel add per touched group; the add that completes a
       // group pushes its WRITE at once — no grid-wide ticket on this path
       __syncthreads();
+      trace_mark_max(rv, 36);  // the last block's rows are stored
       for (int gg = tid; gg < G; gg += blockDim.x) {
         const uint32_t n = s_arr[gg];
         if (n && atom_add_acq_rel_gpu(&sc->llp_grp[0][par][gg], n) + n == (uint32_t)s_gexp[gg])
-          ll_push_dispatch_group(P, lr, gg, s_g0, s_g1, cnt, epoch);
+          ll_push_dispatch_group(P, lr, gg, s_g0, s_g1, epoch);
       }
       // off the critical path: the send-block reuse rule held (one PCIe read)
       if (blockIdx.x == gridDim.x - 1 && tid >= 32 && tid - 32 < G) check_channel_backlog(rv, tid - 32, 2);
@@ -458,7 +484,8 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       // grid width is pinned per context, epb_ll_dispatch)
       if (tid < R) wait_geq(rv, &my_meta->ll_disp_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x600 + tid);
     } else {
-      wait_proxy_groups(rv, my_meta, 0, P.ngroups, P.disp_channels, R, me, P.pthreads, pexp, 0x680);
+      wait_proxy_recv(rv, my_meta, 0, P.ngroups, P.disp_channels, R, me, P.pthreads, pexp, 0x680, P.poll_ns,
+                      P.poll_leader);
     }
     __syncthreads();
     trace_mark(rv, 28);
@@ -549,6 +576,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
 struct LLCombineParams {
   int n_local, phases, use_proxy, disp_channels, pthreads;
   int ngroups;
+  int poll_ns, poll_leader;
   RankView rv[kMaxLocal];
   epb_ll_combine_args_t a[kMaxLocal];
   LLGeom g;
@@ -569,7 +597,8 @@ __device__ __noinline__ void ll_push_combine_group(const LLCombineParams& P, int
     red_release_gpu_add(&sc->llp_self[1], 1u);
     return;
   }
-  fence_sys();
+  trace_mark_max_any(rv, 60);  // (ordering: fifo_push's cumulative release, see the dispatch)
+  trace_mark_max_any(rv, 61);
   const int64_t rel = P.ll_off - (int64_t)kRegionHeader;
   const int64_t first = (int64_t)s_g0[gid] * g.comb_row;
   const int64_t src = rel + g.off_comb_send + (int64_t)(par * R + s) * g.comb_block + first;
@@ -657,6 +686,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
     }
     if (P.use_proxy) {  // report the block's rows to their groups (see the dispatch)
       __syncthreads();
+      trace_mark_max(rv, 37);
       for (int gg = tid; gg < G; gg += blockDim.x) {
         const uint32_t n = s_arr[gg];
         if (n && atom_add_acq_rel_gpu(&sc->llp_grp[1][par][gg], n) + n == (uint32_t)(s_g1[gg] - s_g0[gg]))
@@ -699,7 +729,8 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
     if (!P.use_proxy) {
       if (tid < R) wait_geq(rv, &my_meta->ll_comb_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x700 + tid);
     } else {
-      wait_proxy_groups(rv, my_meta, 1, P.ngroups, P.disp_channels, R, me, P.pthreads, pexp, 0x780);
+      wait_proxy_recv(rv, my_meta, 1, P.ngroups, P.disp_channels, R, me, P.pthreads, pexp, 0x780, P.poll_ns,
+                      P.poll_leader);
     }
     __syncthreads();
     trace_mark(rv, 34);
@@ -834,6 +865,21 @@ static int ll_blocks(epb_t* const* ctxs, int n_local, int num_sms, const void* k
 // default 1): each group is one WRITE the proxy turns into one cudaMemcpyAsync, which
 // costs the host 3-6 us (profiles/r02_ll_proxy.md), so finer groups only pay when the
 // copies are large enough to overlap that cost.
+// Receive polling of the proxy transport: EPB_LL_POLL_NS (sleep between polls,
+// default 200 ns), EPB_LL_POLL_LEADER=1 (block 0 alone polls the signal words).
+static void ll_poll(int* ns, int* leader) {
+  static const int v_ns = [] {
+    const char* s = std::getenv("EPB_LL_POLL_NS");
+    return s ? std::max(0, std::atoi(s)) : 200;
+  }();
+  static const int v_leader = [] {
+    const char* s = std::getenv("EPB_LL_POLL_LEADER");
+    return s ? std::atoi(s) : 0;
+  }();
+  *ns = v_ns;
+  *leader = v_leader;
+}
+
 static int ll_groups(int world, int disp_channels) {
   static const int per = [] {
     const char* s = std::getenv("EPB_LL_GROUPS_PER_RANK");
@@ -875,6 +921,7 @@ extern "C" int epb_ll_dispatch(epb_t* const* ctxs, int n_local, const epb_ll_dis
     if (args[i].num_tokens > args[i].max_tokens) return epb_set_error(EPB_ERR_CONFIG, "num_tokens exceeds max_tokens");
     if (int e = ll_transport(c, P.use_proxy, &P.disp_channels, &P.pthreads)) return e;
     P.ngroups = ll_groups(c->world, P.disp_channels);
+    ll_poll(&P.poll_ns, &P.poll_leader);
     P.rv[i] = c->view();
     P.a[i] = args[i];
   }
@@ -913,6 +960,7 @@ extern "C" int epb_ll_combine(epb_t* const* ctxs, int n_local, const epb_ll_comb
     if (int e = ll_check(c, P.g)) return e;
     if (int e = ll_transport(c, P.use_proxy, &P.disp_channels, &P.pthreads)) return e;
     P.ngroups = ll_groups(c->world, P.disp_channels);
+    ll_poll(&P.poll_ns, &P.poll_leader);
     P.rv[i] = c->view();
     P.a[i] = args[i];
   }
@@ -936,4 +984,12 @@ extern "C" int epb_per_token_cast_to_fp8(const void* x, int num_tokens, int hidd
       static_cast<const __nv_bfloat16*>(x), num_tokens, hidden, round_scale, static_cast<uint8_t*>(q), scales);
   EPB_CUDA(cudaGetLastError());
   return EPB_OK;
+}
+
+// Load this file's kernels now (see epb_preload_kernels, api.cpp).
+cudaError_t epb_preload_ll() {
+  cudaFuncAttributes attr;
+  for (const void* fn : {(const void*)fp8_cast_kernel, (const void*)ll_dispatch_kernel, (const void*)ll_combine_kernel})
+    if (cudaError_t e = cudaFuncGetAttributes(&attr, fn)) return e;
+  return cudaSuccess;
 }

@@ -131,6 +131,13 @@ def main():
             vals = [r[key] for r in rows if r.get(key) is not None]
             med[key] = round(statistics.median(vals), 2) if vals else None
         out[name] = med
+    # kernel-internal marks (us after the phase's kernel start, block 0 unless "last")
+    for name, t0, keys in (("dispatch_marks", 24, {"last_block_start": 39, "bitmap": 30, "counts": 62, "rs_zeroed": 63, "routing_scan": 31,
+                                                   "prologue": 25, "last_block_staged": 36, "block0_done": 26}),
+                           ("combine_marks", 32, {"last_block_staged": 37, "push_entry": 60, "push_fenced": 61,
+                                                  "block0_done": 33})):
+        out[name] = {key: round(statistics.median([(m[i] - m[t0]) / 1e3 for m in calls]), 2) if calls else None
+                     for key, i in keys.items()}
     line = json.dumps(out)
     print(line, flush=True)
     if args.out:
