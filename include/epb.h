@@ -123,6 +123,9 @@ typedef struct {
   int64_t comb_w_off;      /* weights offset inside a combine staging buffer     */
   int64_t slot0_off;       /* offset of slot 0 in the region                     */
   int64_t send_off;        /* proxy transport: send-staging slot offset (else 0) */
+  int64_t comb_flag_off;   /* per-row arrival words inside a combine staging buffer
+                              (streamed push combine: the call epoch, stored after
+                              the row)                                             */
 } epb_recv_layout_t;
 
 int epb_recv_layout(epb_t* ctx, int hidden, int num_topk, epb_recv_layout_t* out);

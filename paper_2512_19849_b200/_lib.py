@@ -50,7 +50,8 @@ class Config(C.Structure):
 class RecvLayout(C.Structure):
     _fields_ = [("cap_rows", i64), ("slot_bytes", i64), ("off_x", i64), ("off_scales", i64),
                 ("off_topk_idx", i64), ("off_topk_w", i64), ("off_src_idx", i64), ("comb_off", i64 * 2),
-                ("comb_w_off", i64), ("slot0_off", i64), ("send_off", i64)]
+                ("comb_w_off", i64), ("slot0_off", i64), ("send_off", i64),
+                ("comb_flag_off", i64)]
 
 
 class DispatchArgs(C.Structure):

@@ -40,6 +40,13 @@ struct CombineParams {
   int seg16;                     // reduce work unit: 16-byte columns per (token, segment); 0 = whole rows
   int tma;                       // reduce from shared memory filled by bulk copies (small SM budgets)
   int tma_seg;                   // bytes per partial per bulk unit
+  int stream;                    // streamed push (R > 1, NVLink): push warps + reduce warps, per-row flags
+  int push_warps;                // stream: warps per block that push (the rest reduce)
+  int push_lanes;                // stream_tma: issuing lanes per push warp (each: one row buffer)
+  int stream_tma;                // stream: rows pushed by bulk copies (HBM -> smem -> peer)
+  int row_pad;                   // stream_tma: bytes per row buffer
+  int flag_rows;                 // stream: rows per arrival word (chunk)
+  int dbg;                       // stream timing decomposition (EPB_COMBINE_DEBUG): 1 no reduce, 2 no row copies
   int bump;                      // this launch ends the call: store the next epoch / done target
                                  // (device-resident, norm_call_begin/_end; the proxy's stage launch does not)
   RankView rv[kMaxLocal];
@@ -418,6 +425,176 @@ __global__ void combine_proxy_wait_kernel(const __grid_constant__ CombineParams 
     wait_geq64(rv, &meta_of(rv.base)->ht_sig[1][tid], P.ht_calls[blockIdx.x], 0x320 + tid, 500);
 }
 
+// Streamed push combine (R > 1 over NVLink).
+// Push and reduce overlap instead of running as two phases around a barrier:
+//   push warps  [0, push_warps): row i of every source o (the i-th row o sent
+//     me) goes back into o's staging at the mirror position, rows taken in
+//     waves i = gw, gw + NW, ... with all sources in lockstep; after each row
+//     lane 0 stores the call epoch into o's arrival word of that row with
+//     st.release.sys (in-band completion: no counter, no barrier);
+//   reduce warps: tokens t = rw, rw + NR, ... (the order the rows arrive in);
+//     lane d waits for the arrival word of d's partial, then the warp reduces
+//     in fp32, ascending rank order, exactly as the two-phase push mode.
+// Peers only write into my staging (never read my memory), and every row a
+// peer writes is awaited by one of my tokens, so no exit barrier is needed.
+__device__ __forceinline__ void wait_epoch_sys(const RankView& rv, const uint32_t* p, uint32_t epoch, int64_t tag) {
+  uint64_t t0 = 0;
+  int iter = 0;
+  while (static_cast<int32_t>(ld_acquire_sys(p) - epoch) < 0) {
+    __nanosleep(64);
+    if ((++iter & 1023) == 0) {
+      const uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > rv.timeout_ns) {
+        report_error(rv, EPB_ERR_DEADLOCK, tag);
+        return;
+      }
+    }
+  }
+}
+
+template <int kMaxFan>
+__device__ __forceinline__ void combine_stream(const CombineParams& P, int lr, const int32_t (*s_cnt)[kMaxRanks],
+                                               const int32_t* s_excl, const int32_t* s_sendpre,
+                                               const int32_t* s_mypre, uint32_t epoch, int par) {
+  const RankView& rv = P.rv[lr];
+  const epb_combine_args_t& a = P.a[lr];
+  const int R = rv.world, me = rv.rank, nb = gridDim.x, b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const int k = a.num_topk, T = a.num_tokens, PW = P.push_warps;
+  const size_t row_bytes = (size_t)a.hidden * 2;
+  const int n16 = (int)(row_bytes >> 4);
+  const char* my_stage = rv.base + P.lay.comb_off[par];
+  __shared__ RowSrc rs;
+  if (tid == 0) rs.row_bytes = row_bytes;
+  if (tid < kMaxRanks) {
+    const int d = tid;
+    rs.base[d] = d == me ? static_cast<const char*>(a.x) : my_stage;
+    rs.wbase[d] = d == me ? reinterpret_cast<const char*>(a.topk_weights) : my_stage + P.lay.comb_w_off;
+    rs.row0[d] = d == me ? s_excl[me] : s_mypre[d];
+  }
+  __syncthreads();
+  // rows go out in chunks of G = flag_rows consecutive rows per source; the
+  // arrival word of a chunk is the one of its last row (one release per chunk:
+  // a release.sys per row cost ~22 us of a 120 us push at EP=2)
+  const int G = P.flag_rows;
+  int nchunk = 0;
+  for (int o = 0; o < R; ++o)
+    if (o != me) nchunk = max(nchunk, (s_cnt[o][me] + G - 1) / G);
+  if (warp < PW && P.stream_tma) {
+    // bulk-copy push: each issuing lane moves whole rows HBM -> its shared
+    // buffer -> the owner's staging with the TMA engine (cp.async.bulk), so
+    // the reduce warps keep the SM's load/store pipeline to themselves
+    const int NL = P.push_lanes;
+    __shared__ __align__(8) uint64_t s_pbar[32];
+    extern __shared__ __align__(128) uint8_t s_prow[];
+    if (lane >= NL) return;
+    const int li = warp * NL + lane;
+    uint8_t* buf = s_prow + (size_t)li * P.row_pad;
+    uint64_t* bar = &s_pbar[li];
+    mbar_init(bar, 1);
+    fence_async_shared();
+    uint32_t phase = 0;
+    const int gi = (b * PW + warp) * NL + lane, NI = nb * PW * NL;
+    for (int c = gi; c < nchunk; c += NI) {
+      for (int o = 0; o < R; ++o) {
+        const int n = s_cnt[o][me], i0 = c * G, i1 = min(n, i0 + G);
+        if (o == me || i0 >= n) continue;
+        char* stage = rv.peer[o] + P.lay.comb_off[par];
+        for (int i = i0; i < i1; ++i) {
+          const size_t drow = (size_t)(s_sendpre[o] + i), srow = (size_t)(s_excl[o] + i);
+          if (P.dbg != 2) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // buffer read out
+            mbar_expect_tx(bar, (uint32_t)row_bytes);
+            bulk_load(buf, static_cast<const char*>(a.x) + srow * row_bytes, (uint32_t)row_bytes, bar);
+            while (!mbar_try_wait(bar, phase)) {
+            }
+            phase ^= 1;
+            bulk_store(stage + drow * row_bytes, buf, (uint32_t)row_bytes);
+            bulk_commit();
+          }
+          if (a.topk_weights != nullptr)
+            for (int q = 0; q < k; ++q)
+              reinterpret_cast<float*>(stage + P.lay.comb_w_off)[drow * k + q] = a.topk_weights[srow * k + q];
+        }
+        bulk_wait_all();  // the chunk's rows are written before its arrival word
+        if (P.dbg != 3)
+          st_release_sys(reinterpret_cast<uint32_t*>(stage + P.lay.comb_flag_off) + s_sendpre[o] + i1 - 1, epoch);
+      }
+    }
+    return;
+  }
+  if (warp < PW) {
+    const int gw = b * PW + warp, NW = nb * PW;
+    for (int c = gw; c < nchunk; c += NW) {
+      for (int o = 0; o < R; ++o) {
+        const int n = s_cnt[o][me], i0 = c * G, i1 = min(n, i0 + G);
+        if (o == me || i0 >= n) continue;
+        char* stage = rv.peer[o] + P.lay.comb_off[par];
+        for (int i = i0; i < i1; ++i) {
+          const size_t drow = (size_t)(s_sendpre[o] + i);
+          const int4* src =
+              reinterpret_cast<const int4*>(static_cast<const char*>(a.x) + (size_t)(s_excl[o] + i) * row_bytes);
+          int4* dst = reinterpret_cast<int4*>(stage + drow * row_bytes);
+          for (int base = 0; base < n16; base += 32 * kCopyUnroll) {
+            int4 v[kCopyUnroll];
+#pragma unroll
+            for (int u = 0; u < kCopyUnroll; ++u) {
+              const int cc = base + u * 32 + lane;
+              if (cc < n16) v[u] = ld_nc_v4(src + cc);
+            }
+#pragma unroll
+            for (int u = 0; u < kCopyUnroll; ++u) {
+              const int cc = base + u * 32 + lane;
+              if (cc < n16) st_v4(dst + cc, v[u]);
+            }
+          }
+          if (a.topk_weights != nullptr && lane < k)
+            reinterpret_cast<float*>(stage + P.lay.comb_w_off)[drow * k + lane] =
+                a.topk_weights[(size_t)(s_excl[o] + i) * k + lane];
+        }
+        __syncwarp();
+        if (lane == 0 && P.dbg != 3)
+          st_release_sys(reinterpret_cast<uint32_t*>(stage + P.lay.comb_flag_off) + s_sendpre[o] + i1 - 1, epoch);
+      }
+    }
+    return;
+  }
+  const int RW = nwarps - PW, rw = b * RW + (warp - PW), NR = nb * RW;
+  const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(my_stage + P.lay.comb_flag_off);
+  if (P.dbg == 3) return;
+  for (int t = rw; t < T; t += NR) {
+    const int32_t* sh = a.send_head + (size_t)t * R;
+    const int shl = lane < R ? sh[lane] : -1;
+    const uint32_t mask = __ballot_sync(0xffffffffu, shl >= 0);
+    if (shl >= 0 && lane != me)  // the arrival word of the chunk holding row shl
+      wait_epoch_sys(rv, my_flags + s_mypre[lane] + min(s_cnt[me][lane], (shl / G + 1) * G) - 1, epoch, 0x3c0 + lane);
+    __syncwarp();
+    int4* out = reinterpret_cast<int4*>(static_cast<char*>(a.combined_x) + (size_t)t * row_bytes);
+    if (P.dbg == 1) continue;
+    switch (__popc(mask)) {
+      case 1: reduce_rows<1>(rs, mask, sh, out, 0, n16, lane); break;
+      case 2: if constexpr (kMaxFan >= 2) reduce_rows<2>(rs, mask, sh, out, 0, n16, lane); break;
+      case 3: if constexpr (kMaxFan >= 3) reduce_rows<3>(rs, mask, sh, out, 0, n16, lane); break;
+      case 4: if constexpr (kMaxFan >= 4) reduce_rows<4>(rs, mask, sh, out, 0, n16, lane); break;
+      case 5: if constexpr (kMaxFan >= 5) reduce_rows<5>(rs, mask, sh, out, 0, n16, lane); break;
+      case 6: if constexpr (kMaxFan >= 6) reduce_rows<6>(rs, mask, sh, out, 0, n16, lane); break;
+      case 7: if constexpr (kMaxFan >= 7) reduce_rows<7>(rs, mask, sh, out, 0, n16, lane); break;
+      case 8: if constexpr (kMaxFan >= 8) reduce_rows<8>(rs, mask, sh, out, 0, n16, lane); break;
+      default: zero_row(out, 0, n16, lane); break;
+    }
+    if (a.combined_topk_weights != nullptr && lane < k) {
+      float w = 0.0f;
+      for (uint32_t m = mask; m != 0; m &= m - 1) {
+        const int d = __ffs(m) - 1;
+        const float* wsrc = reinterpret_cast<const float*>(rs.wbase[d]);
+        if (wsrc != nullptr) w = __fadd_rn(w, wsrc[(size_t)(rs.row0[d] + sh[d]) * k + lane]);
+      }
+      a.combined_topk_weights[(size_t)t * k + lane] = w;
+    }
+  }
+}
+
 template <int kMaxFan>
 __device__ __forceinline__ void combine_body(const CombineParams& P, uint32_t epoch, uint32_t target) {
   const int lr = blockIdx.y;
@@ -461,6 +638,14 @@ __device__ __forceinline__ void combine_body(const CombineParams& P, uint32_t ep
   const bool abort = scratch_of(rv.base)->abort != 0;
   trace_mark(rv, 16);
 
+  if (P.stream && R > 1 && !abort) {
+    combine_stream<kMaxFan>(P, lr, s_cnt, s_excl, s_sendpre, s_mypre, epoch, par);
+    trace_mark(rv, 19);
+    trace_mark_max(rv, 20);
+    __syncthreads();
+    if (tid < R) bump_done(rv, tid, me);  // keeps the cumulative done counters in step (no wait)
+    return;
+  }
   // mode exchange: if every rank's combine input (and weights) lives inside its
   // symmetric region — e.g. the zero-copy recv_x of the dispatch — tokens are
   // reduced by reading the partials in place over NVLink (pull), with no push
@@ -604,6 +789,57 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     return v ? std::atoi(v) : -1;
   }();
   P.seg16 = seg_env >= 0 ? seg_env : 0;
+  // streamed push (combine_stream) for R > 1 over NVLink: opt-in, EPB_COMBINE_MODE=stream.
+  // Parity-green but slower than the pull reduce at EP=2 (128.6 us against 119.4 us
+  // per combine; push alone 99 us without arrival words, 121 us with one per row;
+  // profiles/r02_combine_stream_n2.txt).  EPB_COMBINE_PUSH_WARPS = push warps per block
+  static const int mode_env = [] {
+    const char* v = std::getenv("EPB_COMBINE_MODE");
+    if (!v) return -1;
+    return std::strcmp(v, "stream") == 0 ? 1 : 0;
+  }();
+  static const int pw_env = [] {
+    const char* v = std::getenv("EPB_COMBINE_PUSH_WARPS");
+    return v ? std::atoi(v) : 1;
+  }();
+  P.stream = (!P.proxy && ctxs[0]->world > 1 && mode_env == 1) ? 1 : 0;
+  P.push_warps = std::max(1, std::min(threads / 32 - 1, pw_env));
+  // stream: bulk-copy pushers (EPB_COMBINE_STREAM_TMA=0 off; EPB_COMBINE_PUSH_LANES
+  // issuing lanes per push warp, each with one row buffer in shared memory)
+  static const int stma_env = [] {
+    const char* v = std::getenv("EPB_COMBINE_STREAM_TMA");
+    return v ? std::atoi(v) : 1;
+  }();
+  static const int pl_env = [] {
+    const char* v = std::getenv("EPB_COMBINE_PUSH_LANES");
+    return v ? std::atoi(v) : 8;
+  }();
+  static const int dbg_env = [] {
+    const char* v = std::getenv("EPB_COMBINE_DEBUG");
+    return v ? std::atoi(v) : 0;
+  }();
+  P.dbg = dbg_env;
+  static const int fr_env = [] {
+    const char* v = std::getenv("EPB_COMBINE_FLAG_ROWS");
+    return v ? std::atoi(v) : 2;
+  }();
+  P.flag_rows = std::max(1, fr_env);
+  size_t stream_smem = 0;
+  if (P.stream && stma_env > 0) {
+    const size_t rb = (size_t)args[0].hidden * 2;
+    bool ok = rb % 16 == 0;
+    for (int i = 0; i < n_local && ok; ++i)
+      ok = (size_t)args[i].hidden * 2 == rb && (reinterpret_cast<uintptr_t>(args[i].x) & 15) == 0;
+    P.push_lanes = std::max(1, std::min(32 / P.push_warps, pl_env));
+    P.row_pad = (int)((rb + 127) & ~(size_t)127);
+    stream_smem = (size_t)P.push_warps * P.push_lanes * P.row_pad;
+    if (ok && stream_smem <= 200 * 1024) {
+      P.stream_tma = 1;
+      EPB_CUDA(epb_ensure_smem(kern, stream_smem));
+    } else {
+      stream_smem = 0;
+    }
+  }
   // bulk-copy reduce: opt-in only (EPB_TMA=1).  Parity-green, but measured slower
   // than the register path at every SM budget (N=1, 20/24/48 SMs: 280/239/124 us
   // against 76/66/38 us; profiles/r02_tma_ab_n1.txt): 4 warps x 3 stages of
@@ -632,6 +868,7 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
       EPB_CUDA(epb_ensure_smem(kern, smem));
     }
   }
+  smem = std::max(smem, stream_smem);
   const int max_active = epb_max_active_blocks(kern, threads, smem);
   nb = std::min(nb, std::max(1, max_active * ctxs[0]->num_sms / n_local));
   for (int i = 0; i < n_local; ++i) {

@@ -186,7 +186,7 @@ int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t
   const size_t S = (size_t)hidden / 128;
   const size_t x_row = 2 * (size_t)hidden;
   const size_t per_row = x_row + S * 4 + (size_t)k * 12 + 4;
-  const size_t comb_row = 2 * (size_t)hidden + (size_t)k * 4;
+  const size_t comb_row = 2 * (size_t)hidden + (size_t)k * 4 + 4;
   const int ns = std::max(1, ctx->cfg.num_recv_slots);
   const int nsend = ctx->cfg.ht_transport == EPB_HT_PROXY ? 1 : 0;  // proxy transport: one send-staging slot
   const size_t overhead = A * (size_t)(6 * (ns + nsend) + 6);
@@ -203,8 +203,10 @@ int compute_recv_layout(const epb_ctx* ctx, int hidden, int k, epb_recv_layout_t
   L->off_src_idx = align_up(L->off_topk_w + cap * (size_t)k * 4, A);
   L->slot_bytes = align_up(L->off_src_idx + cap * 4, A);
   L->slot0_off = ctx->arena_off();
-  const int64_t comb_bytes = align_up(cap * 2 * (size_t)hidden, A) + align_up(cap * (size_t)k * 4, A);
+  const int64_t comb_bytes =
+      align_up(cap * 2 * (size_t)hidden, A) + align_up(cap * (size_t)k * 4, A) + align_up(cap * 4, A);
   L->comb_w_off = align_up(cap * 2 * (size_t)hidden, A);
+  L->comb_flag_off = L->comb_w_off + align_up(cap * (size_t)k * 4, A);
   L->comb_off[0] = L->slot0_off + ns * L->slot_bytes;
   L->comb_off[1] = L->comb_off[0] + comb_bytes;
   L->send_off = nsend ? L->comb_off[1] + comb_bytes : 0;
