@@ -25,6 +25,7 @@ namespace epb {
 constexpr int kCombineThreadsSolo = 512;
 constexpr int kCombineThreads = 256;
 constexpr int kCopyUnroll = 7;
+constexpr int kStreamAutoBlocks = 48;  // streamed push combine at <= this many blocks per rank
 // ---------------------------------------------------------------------------
 // combine: cooperative grid.  Phase A pushes each received row back into its
 // source's staging at the mirror of the dispatch position; phase B (after a
@@ -40,7 +41,8 @@ struct CombineParams {
   int seg16;                     // reduce work unit: 16-byte columns per (token, segment); 0 = whole rows
   int tma;                       // reduce from shared memory filled by bulk copies (small SM budgets)
   int tma_seg;                   // bytes per partial per bulk unit
-  int stream;                    // streamed push (R > 1, NVLink): push warps + reduce warps, per-row flags
+  int stream;                    // streamed push (R > 1, NVLink): 1 = always, 2 = in place of a two-phase push
+  int force_push;                // two-phase push even when every input lives in its region
   int push_warps;                // stream: warps per block that push (the rest reduce)
   int push_lanes;                // stream_tma: issuing lanes per push warp (each: one row buffer)
   int stream_tma;                // stream: rows pushed by bulk copies (HBM -> smem -> peer)
@@ -638,7 +640,7 @@ __device__ __forceinline__ void combine_body(const CombineParams& P, uint32_t ep
   const bool abort = scratch_of(rv.base)->abort != 0;
   trace_mark(rv, 16);
 
-  if (P.stream && R > 1 && !abort) {
+  if (P.stream == 1 && R > 1 && !abort) {
     combine_stream<kMaxFan>(P, lr, s_cnt, s_excl, s_sendpre, s_mypre, epoch, par);
     trace_mark(rv, 19);
     trace_mark_max(rv, 20);
@@ -688,8 +690,16 @@ __device__ __forceinline__ void combine_body(const CombineParams& P, uint32_t ep
     else s_xoff[s] = off;
   }
   __syncthreads();
-  bool pull = true;
+  bool pull = !P.force_push;
   for (int d = 0; d < R; ++d) pull = pull && s_xoff[d] >= 0;
+  if (!pull && !abort && P.stream == 2) {  // some input outside its region: streamed push
+    combine_stream<kMaxFan>(P, lr, s_cnt, s_excl, s_sendpre, s_mypre, epoch, par);
+    trace_mark(rv, 19);
+    trace_mark_max(rv, 20);
+    __syncthreads();
+    if (tid < R) bump_done(rv, tid, me);
+    return;
+  }
 
   // phase A (push mode): push rows back to their sources
   const int Jb = (N + nb - 1) / nb;
@@ -789,20 +799,28 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     return v ? std::atoi(v) : -1;
   }();
   P.seg16 = seg_env >= 0 ? seg_env : 0;
-  // streamed push (combine_stream) for R > 1 over NVLink: opt-in, EPB_COMBINE_MODE=stream.
-  // Parity-green but slower than the pull reduce at EP=2 (128.6 us against 119.4 us
-  // per combine; push alone 99 us without arrival words, 121 us with one per row;
-  // profiles/r02_combine_stream_n2.txt).  EPB_COMBINE_PUSH_WARPS = push warps per block
+  // streamed push (combine_stream) for R > 1 over NVLink.  Auto (EPB_COMBINE_MODE
+  // unset): always on small SM budgets (<= kStreamAutoBlocks blocks per rank: 252
+  // against 500 us at 20 SMs, EP=2) and in place of the two-phase push when some
+  // input lives outside its region (134 against 148 us); with every input in its
+  // region at full width the pull reduce stays (119 against 127 us;
+  // profiles/r02_combine_stream_n2.txt).  EPB_COMBINE_MODE=stream | classic | push
+  // forces stream / never stream / the two-phase push.  EPB_COMBINE_PUSH_WARPS = push warps per block
   static const int mode_env = [] {
     const char* v = std::getenv("EPB_COMBINE_MODE");
     if (!v) return -1;
-    return std::strcmp(v, "stream") == 0 ? 1 : 0;
+    return std::strcmp(v, "stream") == 0 ? 1 : std::strcmp(v, "push") == 0 ? 2 : 0;
   }();
   static const int pw_env = [] {
     const char* v = std::getenv("EPB_COMBINE_PUSH_WARPS");
     return v ? std::atoi(v) : 1;
   }();
-  P.stream = (!P.proxy && ctxs[0]->world > 1 && mode_env == 1) ? 1 : 0;
+  P.stream = 0;
+  if (!P.proxy && ctxs[0]->world > 1) {
+    if (mode_env == 1) P.stream = 1;
+    else if (mode_env < 0) P.stream = nb <= kStreamAutoBlocks ? 1 : 2;
+  }
+  P.force_push = mode_env == 2 ? 1 : 0;
   P.push_warps = std::max(1, std::min(threads / 32 - 1, pw_env));
   // stream: bulk-copy pushers (EPB_COMBINE_STREAM_TMA=0 off; EPB_COMBINE_PUSH_LANES
   // issuing lanes per push warp, each with one row buffer in shared memory)
@@ -887,7 +905,7 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
     EPB_CUDA(cudaLaunchKernel(kern, dim3(nb, n_local), dim3(threads), kargs, 0, st));
     combine_proxy_wait_kernel<<<n_local, 32, 0, st>>>(P);
     EPB_CUDA(cudaGetLastError());
-    if (!std::getenv("EPB_PROXY_ASYNC")) EPB_CUDA(cudaStreamSynchronize(st));  // see epb_dispatch
+    if (std::getenv("EPB_PROXY_SYNC")) EPB_CUDA(cudaStreamSynchronize(st));  // see epb_dispatch
     P.phase = 2;
     P.bump = 1;
     EPB_CUDA(cudaLaunchKernel(kern, dim3(nb, n_local), dim3(threads), kargs, 0, st));

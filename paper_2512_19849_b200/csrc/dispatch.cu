@@ -912,10 +912,10 @@ static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_a
   if (P.proxy) {
     dispatch_proxy_wait_kernel<<<n_local, 32, 0, st>>>(P);
     EPB_CUDA(cudaGetLastError());
-    // the host does not run ahead of the wait: work enqueued behind a wait
-    // kernel that spins on the proxy's copies was seen to hold those copies
-    // back until the wait timed out (NCCL jobs, tools/proxy_ht_check.py)
-    if (!std::getenv("EPB_PROXY_ASYNC")) EPB_CUDA(cudaStreamSynchronize(st));
+    // no host sync: the stall that once held the proxy's copies behind work
+    // enqueued after this wait was the lazy load of the next kernel (fixed by
+    // epb_create's kernel preload); EPB_PROXY_SYNC=1 restores the sync
+    if (std::getenv("EPB_PROXY_SYNC")) EPB_CUDA(cudaStreamSynchronize(st));
   }
   return EPB_OK;
 }
