@@ -801,10 +801,11 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
   P.seg16 = seg_env >= 0 ? seg_env : 0;
   // streamed push (combine_stream) for R > 1 over NVLink.  Auto (EPB_COMBINE_MODE
   // unset): always on small SM budgets (<= kStreamAutoBlocks blocks per rank: 252
-  // against 500 us at 20 SMs, EP=2) and in place of the two-phase push when some
-  // input lives outside its region (134 against 148 us); with every input in its
-  // region at full width the pull reduce stays (119 against 127 us;
-  // profiles/r02_combine_stream_n2.txt).  EPB_COMBINE_MODE=stream | classic | push
+  // against 500 us at 20 SMs at EP=2, 558 against 1044 us at EP=4) and, at EP=2
+  // only, in place of the two-phase push when some input lives outside its region
+  // (134 against 148 us; at EP=4 520 against 332 us).  With every input in its
+  // region at full width the pull reduce stays (EP=2 119 against 127 us, EP=4 286
+  // against 444 us; profiles/r02_combine_stream_n2.txt, r02_combine_stream_n4.txt).  EPB_COMBINE_MODE=stream | classic | push
   // forces stream / never stream / the two-phase push.  EPB_COMBINE_PUSH_WARPS = push warps per block
   static const int mode_env = [] {
     const char* v = std::getenv("EPB_COMBINE_MODE");
@@ -818,7 +819,7 @@ extern "C" int epb_combine(epb_t* const* ctxs, int n_local, const epb_combine_ar
   P.stream = 0;
   if (!P.proxy && ctxs[0]->world > 1) {
     if (mode_env == 1) P.stream = 1;
-    else if (mode_env < 0) P.stream = nb <= kStreamAutoBlocks ? 1 : 2;
+    else if (mode_env < 0) P.stream = nb <= kStreamAutoBlocks ? 1 : ctxs[0]->world == 2 ? 2 : 0;
   }
   P.force_push = mode_env == 2 ? 1 : 0;
   P.push_warps = std::max(1, std::min(threads / 32 - 1, pw_env));
