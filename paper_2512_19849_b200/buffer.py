@@ -136,6 +136,8 @@ def default_proxy_threads() -> int:
      when the host has the cores, else what this rank's share of
     the cores leaves after its main thread (the threads spin while work is in
     flight, so oversubscribing cores stalls them for scheduler time slices)."""
+    if os.environ.get("EPB_PROXY_THREADS"):
+        return max(1, int(os.environ["EPB_PROXY_THREADS"]))
     cores = len(os.sched_getaffinity(0))
     ranks_here = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
     return max(1, min(4, cores // max(1, ranks_here) - 1))

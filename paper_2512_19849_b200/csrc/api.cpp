@@ -157,6 +157,7 @@ extern "C" int epb_create(epb_t** out, int rank, int world, const epb_config_t* 
   if (ctx->cfg.num_recv_slots <= 0) ctx->cfg.num_recv_slots = 2;
   if (const char* s = std::getenv("EPB_TIMEOUT_S")) ctx->timeout_ns = (uint64_t)(std::atof(s) * 1e9);
   if (const char* s = std::getenv("EPB_TRACE")) ctx->trace = std::atoi(s) != 0;
+  if (const char* s = std::getenv("EPB_PROXY_CHMAP")) ctx->proxy_chmap = std::strcmp(s, "phase") == 0 ? 1 : 0;
   cudaError_t e = cudaGetDevice(&ctx->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
   if (e == cudaSuccess) e = epb_preload_kernels(ctx->device);

@@ -131,6 +131,22 @@ constexpr size_t kMetaBytes = align_up(sizeof(Meta), 4096);
 constexpr size_t kScratchBytes = align_up(sizeof(Scratch), 4096);
 constexpr size_t kRegionHeader = kMetaBytes + kScratchBytes;
 
+#ifdef __CUDACC__
+#define EPB_HD __host__ __device__
+#else
+#define EPB_HD
+#endif
+// FIFO channel -> CPU proxy thread, shared by the proxy (which channels a thread
+// serves) and the LL receivers (whose signal words to wait on).  0: c % nth.
+// 1 ("phase", EPB_PROXY_CHMAP=phase): every channel of the first half (LL
+// dispatch) on thread 0, of the second half (LL combine) on thread 1 % nth, so
+// one thread sees all of a phase's commands in one sweep and issues them together.
+EPB_HD inline int proxy_thread_of(int ch, int half, int nth, int mode) {
+  if (mode == 1) return ch < half ? 0 : 1 % nth;
+  return ch % nth;
+}
+
+
 // Pinned, device-mapped host words the kernels publish to the CPU.
 // The dispatch publishes the receive counts to the host as tagged words, so
 // the host needs no flag and the kernel no system-scope fence (a fence.sys

@@ -24,6 +24,7 @@ struct epb_ctx {
   uint64_t ht_disp_calls = 0, ht_comb_calls = 0;  // proxy transport calls so far (ht_sig targets)
   uint64_t ll_proxy_disp = 0, ll_proxy_comb = 0;  // proxy-transport LL calls so far (signal targets)
   int num_sms = 148;
+  int proxy_chmap = 0;                  // proxy_thread_of mode (EPB_PROXY_CHMAP=phase -> 1)
   uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;
   int trace = 0;                        // EPB_TRACE=1: kernels record phase timestamps
   int ll_grid[2] = {0, 0};              // LL dispatch / combine grid width, pinned at the first call
@@ -64,6 +65,31 @@ int epb_max_active_blocks(const void* func, int threads, size_t smem);
 cudaError_t epb_ensure_smem(const void* func, size_t smem);
 void epb_set_carveout(const void* func, bool enable = true);
 bool epb_carveout_skip(const char* name);
+
+// SM copy engine of the CPU proxy (EPB_PROXY_ENGINE=sm; fifo.cu): the proxy
+// thread launches one copy kernel per sweep instead of copy-engine copies.  A
+// job = contiguous segments to one destination, then an optional stream-ordered
+// 8-byte signal (the piggybacked count / ATOMIC value), written by the job's
+// last block after every block's copies.
+struct epb_pcopy_seg {
+  const char* src;
+  char* dst;
+  uint64_t len;
+};
+struct epb_pcopy_job {
+  int seg0, nseg, blocks, block0;
+  uint64_t* sig;      // nullptr: no signal
+  uint64_t sig_val;
+};
+constexpr int kPcopyJobs = 8, kPcopySegs = 16;  // small launch parameters (~0.7 KB)
+struct epb_pcopy_batch {
+  int njobs, nsegs, nblocks;
+  uint32_t* tickets;  // [kPcopyJobs] device counters, zero between launches
+  int64_t* stamp;     // tracing: [2] = %globaltimer at kernel start, at the last signal (or nullptr)
+  epb_pcopy_job jobs[kPcopyJobs];
+  epb_pcopy_seg segs[kPcopySegs];
+};
+cudaError_t epb_pcopy_launch(const epb_pcopy_batch& b, cudaStream_t st);
 
 // Per-file kernel preloads (each .cu), run once per device by epb_create.
 cudaError_t epb_preload_ll();

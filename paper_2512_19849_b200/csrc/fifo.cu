@@ -14,6 +14,55 @@
 
 namespace epb {
 
+// The proxy's SM copy engine (epb_pcopy_batch, ctx.h): blocks [block0, block0 +
+// blocks) of a job split each of its segments into contiguous 16-byte ranges
+// (ld.global.nc + plain stores, over NVLink for a peer destination); the last
+// block of the job (a ticket) publishes its signal with st.release.sys after a
+// fence that orders every block's copies (release fence + relaxed RMW pattern).
+__global__ void __launch_bounds__(512) pcopy_kernel(const __grid_constant__ epb_pcopy_batch B) {
+  if (B.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) B.stamp[0] = (int64_t)globaltimer();
+  int j = 0;
+  while (j + 1 < B.njobs && (int)blockIdx.x >= B.jobs[j + 1].block0) ++j;
+  const epb_pcopy_job& J = B.jobs[j];
+  const int bj = blockIdx.x - J.block0, nbj = J.blocks;
+  for (int s = J.seg0; s < J.seg0 + J.nseg; ++s) {
+    const epb_pcopy_seg& g = B.segs[s];
+    if (((reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst)) & 15) != 0) {
+      // unaligned segment (e.g. a weights array): bytes, strided over the job's blocks
+      for (uint64_t i = (uint64_t)bj * blockDim.x + threadIdx.x; i < g.len; i += (uint64_t)nbj * blockDim.x)
+        g.dst[i] = g.src[i];
+      continue;
+    }
+    const uint64_t n16 = g.len >> 4;
+    const uint64_t u0 = n16 * bj / nbj, u1 = n16 * (bj + 1) / nbj;
+    const int4* src = reinterpret_cast<const int4*>(g.src);
+    int4* dst = reinterpret_cast<int4*>(g.dst);
+    uint64_t u = u0 + threadIdx.x;
+    for (; u + 3 * blockDim.x < u1; u += 4 * blockDim.x) {
+      const int4 v0 = ld_nc_v4(src + u), v1 = ld_nc_v4(src + u + blockDim.x);
+      const int4 v2 = ld_nc_v4(src + u + 2 * blockDim.x), v3 = ld_nc_v4(src + u + 3 * blockDim.x);
+      st_v4(dst + u, v0);
+      st_v4(dst + u + blockDim.x, v1);
+      st_v4(dst + u + 2 * blockDim.x, v2);
+      st_v4(dst + u + 3 * blockDim.x, v3);
+    }
+    for (; u < u1; u += blockDim.x) st_v4(dst + u, ld_nc_v4(src + u));
+    if (bj == nbj - 1 && threadIdx.x < (g.len & 15))  // tail bytes
+      g.dst[(n16 << 4) + threadIdx.x] = g.src[(n16 << 4) + threadIdx.x];
+  }
+  if (J.sig == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_sys();
+    if (atomicAdd(&B.tickets[j], 1u) == (uint32_t)nbj - 1) {
+      B.tickets[j] = 0;
+      fence_sys();
+      st_release_sys(J.sig, J.sig_val);
+      if (B.stamp != nullptr) atomicMax(reinterpret_cast<unsigned long long*>(&B.stamp[1]), (unsigned long long)globaltimer());
+    }
+  }
+}
+
 __global__ void fifo_bench_kernel(RankView rv, int64_t n_per_ch, int channels, int64_t* elapsed) {
   const int ch = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (ch >= channels) return;
@@ -299,10 +348,16 @@ extern "C" int epb_debug_stamp(int64_t* dst, void* stream) {
   return EPB_OK;
 }
 
+cudaError_t epb_pcopy_launch(const epb_pcopy_batch& b, cudaStream_t st) {
+  if (b.njobs == 0) return cudaSuccess;
+  epb::pcopy_kernel<<<b.nblocks, 512, 0, st>>>(b);
+  return cudaGetLastError();
+}
+
 // Load this file's kernels now (see epb_preload_kernels, api.cpp).
 cudaError_t epb_preload_fifo() {
   cudaFuncAttributes attr;
-  for (const void* fn : {(const void*)fifo_bench_kernel, (const void*)proxy_barrier_kernel, (const void*)epb::proxy_drain_kernel, (const void*)epb::drain_test_kernel, (const void*)epb::stamp_kernel, (const void*)epb::clock_beacon_kernel})
+  for (const void* fn : {(const void*)epb::pcopy_kernel, (const void*)fifo_bench_kernel, (const void*)proxy_barrier_kernel, (const void*)epb::proxy_drain_kernel, (const void*)epb::drain_test_kernel, (const void*)epb::stamp_kernel, (const void*)epb::clock_beacon_kernel})
     if (cudaError_t e = cudaFuncGetAttributes(&attr, fn)) return e;
   return cudaSuccess;
 }

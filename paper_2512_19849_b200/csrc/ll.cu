@@ -111,10 +111,11 @@ __device__ __forceinline__ int group_of_row(const int32_t* s_g1, int G, int R, i
 }
 
 // Receiver side: piggybacked WRITEs from src's proxy thread pt to me per call
-// (group b goes to rank b % R on channel chan0 + b, served by thread chan % nth).
-__device__ __forceinline__ int proxy_cmds_per_call(int G, int R, int me, int chan0, int nth, int pt) {
+// (group b goes to rank b % R on channel chan0 + b, served by proxy_thread_of).
+__device__ __forceinline__ int proxy_cmds_per_call(int G, int R, int me, int chan0, int half, int nth, int mode,
+                                                   int pt) {
   int n = 0;
-  for (int b = me; b < G; b += R) n += ((chan0 + b) % nth) == pt;
+  for (int b = me; b < G; b += R) n += proxy_thread_of(chan0 + b, half, nth, mode) == pt;
   return n;
 }
 
@@ -122,7 +123,8 @@ __device__ __forceinline__ int proxy_cmds_per_call(int G, int R, int me, int cha
 // (my own rows never go through the proxy: they were stored locally and
 // counted on Scratch::llp_self — one add per group, G / R groups per call)
 __device__ __forceinline__ void wait_proxy_groups(const RankView& rv, const Meta* my, int kind, int G, int half, int R,
-                                                  int me, int nth, uint64_t calls, int64_t tag, unsigned poll_ns) {
+                                                  int me, int nth, int chmap, uint64_t calls, int64_t tag,
+                                                  unsigned poll_ns) {
   for (int i = threadIdx.x; i < R * nth; i += blockDim.x) {
     const int s = i / nth, pt = i % nth;
     if (s == me) {
@@ -130,7 +132,7 @@ __device__ __forceinline__ void wait_proxy_groups(const RankView& rv, const Meta
         wait_geq_gpu(rv, &scratch_of(rv.base)->llp_self[kind], (uint32_t)(calls * (uint64_t)(G / R)), tag + i);
       continue;
     }
-    const int n = proxy_cmds_per_call(G, R, me, kind ? half : 0, nth, pt);
+    const int n = proxy_cmds_per_call(G, R, me, kind ? half : 0, half, nth, chmap, pt);
     if (n > 0) wait_geq64(rv, &my->proxy_sig[kind * 32 + pt][s], calls * (uint64_t)n, tag + i, poll_ns);
   }
 }
@@ -140,14 +142,15 @@ __device__ __forceinline__ void wait_proxy_groups(const RankView& rv, const Meta
 // the copy engines write) and releases the call count to the other blocks.
 // The caller synchronises the block afterwards.
 __device__ __forceinline__ void wait_proxy_recv(const RankView& rv, const Meta* my, int kind, int G, int half, int R,
-                                                int me, int nth, uint64_t calls, int64_t tag, int poll_ns, int leader) {
+                                                int me, int nth, int chmap, uint64_t calls, int64_t tag, int poll_ns,
+                                                int leader) {
   if (!leader) {
-    wait_proxy_groups(rv, my, kind, G, half, R, me, nth, calls, tag, (unsigned)poll_ns);
+    wait_proxy_groups(rv, my, kind, G, half, R, me, nth, chmap, calls, tag, (unsigned)poll_ns);
     return;
   }
   Scratch* sc = scratch_of(rv.base);
   if (blockIdx.x == 0) {
-    wait_proxy_groups(rv, my, kind, G, half, R, me, nth, calls, tag, (unsigned)poll_ns);
+    wait_proxy_groups(rv, my, kind, G, half, R, me, nth, chmap, calls, tag, (unsigned)poll_ns);
     __syncthreads();
     if (threadIdx.x == 0) st_release_gpu(&sc->llp_go[kind], (uint32_t)calls);
   } else if (threadIdx.x == 0) {
@@ -162,6 +165,7 @@ struct LLDispatchParams {
   int n_local, phases, use_proxy, disp_channels, pthreads;
   int ngroups;  // proxy transport: command groups (R x groups per destination, <= disp_channels)
   int poll_ns, poll_leader;  // proxy transport receive polling (ll_poll)
+  int chmap;                 // proxy_thread_of mode of the channels' proxy threads
   RankView rv[kMaxLocal];
   epb_ll_dispatch_args_t a[kMaxLocal];
   LLGeom g;
@@ -484,8 +488,8 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_dispatch_kernel(const __grid
       // grid width is pinned per context, epb_ll_dispatch)
       if (tid < R) wait_geq(rv, &my_meta->ll_disp_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x600 + tid);
     } else {
-      wait_proxy_recv(rv, my_meta, 0, P.ngroups, P.disp_channels, R, me, P.pthreads, pexp, 0x680, P.poll_ns,
-                      P.poll_leader);
+      wait_proxy_recv(rv, my_meta, 0, P.ngroups, P.disp_channels, R, me, P.pthreads, P.chmap, pexp, 0x680,
+                      P.poll_ns, P.poll_leader);
     }
     __syncthreads();
     trace_mark(rv, 28);
@@ -577,6 +581,7 @@ struct LLCombineParams {
   int n_local, phases, use_proxy, disp_channels, pthreads;
   int ngroups;
   int poll_ns, poll_leader;
+  int chmap;
   RankView rv[kMaxLocal];
   epb_ll_combine_args_t a[kMaxLocal];
   LLGeom g;
@@ -729,8 +734,8 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_combine_kernel(const __grid_
     if (!P.use_proxy) {
       if (tid < R) wait_geq(rv, &my_meta->ll_comb_cnt[par][tid], ((epoch + 1u) >> 1) * gridDim.x, 0x700 + tid);
     } else {
-      wait_proxy_recv(rv, my_meta, 1, P.ngroups, P.disp_channels, R, me, P.pthreads, pexp, 0x780, P.poll_ns,
-                      P.poll_leader);
+      wait_proxy_recv(rv, my_meta, 1, P.ngroups, P.disp_channels, R, me, P.pthreads, P.chmap, pexp, 0x780,
+                      P.poll_ns, P.poll_leader);
     }
     __syncthreads();
     trace_mark(rv, 34);
@@ -922,6 +927,7 @@ extern "C" int epb_ll_dispatch(epb_t* const* ctxs, int n_local, const epb_ll_dis
     if (int e = ll_transport(c, P.use_proxy, &P.disp_channels, &P.pthreads)) return e;
     P.ngroups = ll_groups(c->world, P.disp_channels);
     ll_poll(&P.poll_ns, &P.poll_leader);
+    P.chmap = c->proxy_chmap;
     P.rv[i] = c->view();
     P.a[i] = args[i];
   }
@@ -961,6 +967,7 @@ extern "C" int epb_ll_combine(epb_t* const* ctxs, int n_local, const epb_ll_comb
     if (int e = ll_transport(c, P.use_proxy, &P.disp_channels, &P.pthreads)) return e;
     P.ngroups = ll_groups(c->world, P.disp_channels);
     ll_poll(&P.poll_ns, &P.poll_leader);
+    P.chmap = c->proxy_chmap;
     P.rv[i] = c->view();
     P.a[i] = args[i];
   }

@@ -127,10 +127,29 @@ struct Inflight {
   std::vector<std::pair<int, int64_t>> marks;  // (channel, COMPLETED value) once evs are done
 };
 
+// SM copy engine (EPB_PROXY_ENGINE=sm): a destination's pending copies and up
+// to two signals, turned into one job of the sweep's copy-kernel launch
+struct PJob {
+  int dest = -1;
+  std::vector<epb_pcopy_seg> segs;
+  uint64_t* sig[2] = {nullptr, nullptr};
+  uint64_t val[2] = {0, 0};
+  int nsig = 0;
+  uint64_t bytes = 0;
+};
+
 struct Worker {
   epb_proxy* px;
   epb_ctx* ctx;
   int tid, nthreads, half;
+  bool sm_engine = false;
+  cudaStream_t kst = nullptr;     // SM engine: the thread's copy-kernel stream
+  bool kst_used = false;
+  uint32_t* tickets = nullptr;    // SM engine: per-job last-block tickets (device)
+  int64_t* stamps = nullptr;      // SM engine + tracing: [kStampRing][2] device stamps per launch
+  int64_t launches = 0;
+  static constexpr int kStampRing = 512;
+  std::vector<PJob> jobs;         // SM engine: the sweep's open jobs, in issue order
   std::vector<ChanState> chans;
   std::vector<DestState> dests;
   std::unordered_map<uint64_t, uint64_t> shadow;  // ATOMIC counters: (dst, off) -> cumulative value
@@ -167,9 +186,96 @@ struct Worker {
     return ev;
   }
 
+  // SM engine: the open job of destination d (a job that already carries a
+  // signal takes no more copies: its signal must follow only its own copies)
+  PJob& job_for(int d, bool for_copy) {
+    for (int i = (int)jobs.size() - 1; i >= 0; --i)
+      if (jobs[i].dest == d) {
+        if ((for_copy && jobs[i].nsig > 0) || jobs[i].nsig == 2) break;
+        return jobs[i];
+      }
+    if (jobs.size() >= (size_t)kPcopyJobs) launch_jobs();
+    jobs.emplace_back();
+    jobs.back().dest = d;
+    return jobs.back();
+  }
+  // one copy-kernel launch for the open jobs (several if they exceed a batch)
+  int64_t* next_stamp() {
+    if (!stamps) return nullptr;
+    int64_t* p = stamps + 2 * (launches % kStampRing);
+    ++launches;
+    return p;
+  }
+  void launch_jobs() {
+    size_t i = 0;
+    while (i < jobs.size()) {
+      epb_pcopy_batch b;
+      std::memset(&b, 0, sizeof(b));
+      b.tickets = tickets;
+      b.stamp = next_stamp();
+      // a destination's later job must not run beside its earlier one (its
+      // signal could overtake the earlier copies): one job per destination per launch
+      bool seen[epb::kMaxRanks] = {};
+      while (i < jobs.size() && b.njobs < kPcopyJobs && !seen[jobs[i].dest] &&
+             b.nsegs + (int)jobs[i].segs.size() <= kPcopySegs) {
+        const PJob& J = jobs[i];
+        seen[J.dest] = true;
+        epb_pcopy_job& q = b.jobs[b.njobs];
+        q.seg0 = b.nsegs;
+        q.nseg = (int)J.segs.size();
+        for (const epb_pcopy_seg& g : J.segs) b.segs[b.nsegs++] = g;
+        q.blocks = (int)std::min<uint64_t>(32, std::max<uint64_t>(1, J.bytes >> 16));
+        q.block0 = b.nblocks;
+        b.nblocks += q.blocks;
+        q.sig = J.nsig > 0 ? J.sig[0] : nullptr;
+        q.sig_val = J.val[0];
+        if (J.nsig > 0) tr(3, J.dest, (int64_t)J.val[0]);
+        ++b.njobs;
+        if (J.nsig == 2) {  // the second signal: a copy-free job right behind (next launch)
+          ++i;
+          tr(6, -1, (int64_t)b.nblocks);
+          ok(epb_pcopy_launch(b, kst));
+          std::memset(&b, 0, sizeof(b));
+          b.tickets = tickets;
+          b.stamp = next_stamp();
+          epb_pcopy_job& q2 = b.jobs[0];
+          q2.blocks = 1;
+          q2.sig = J.sig[1];
+          q2.sig_val = J.val[1];
+          tr(3, J.dest, (int64_t)J.val[1]);
+          b.njobs = 1;
+          b.nblocks = 1;
+          tr(6, -2, 1);
+          ok(epb_pcopy_launch(b, kst));
+          std::memset(&b, 0, sizeof(b));
+          b.tickets = tickets;
+          b.stamp = next_stamp();
+          break;
+        }
+        ++i;
+      }
+      if (b.njobs > 0) {
+        tr(6, -1, (int64_t)b.nblocks);
+        ok(epb_pcopy_launch(b, kst));
+      }
+      px->copies.fetch_add(1, std::memory_order_relaxed);
+      tr(2, -1, 0);
+    }
+    jobs.clear();
+    kst_used = true;
+  }
+
   void flush(int d) {
     DestState& ds = dests[d];
     if (ds.pend.len == 0) return;
+    if (sm_engine) {
+      PJob& J = job_for(d, true);
+      J.segs.push_back({ds.pend.src, ds.pend.dstp, (uint64_t)ds.pend.len});
+      J.bytes += ds.pend.len;
+      if (J.segs.size() >= (size_t)kPcopySegs / 2) launch_jobs();
+      ds.pend = PendingCopy{};
+      return;
+    }
     tr(6, d, (int64_t)ds.pend.len);
     ok(cudaMemcpyAsync(ds.pend.dstp, ds.pend.src, ds.pend.len, cudaMemcpyDefault, ds.st));
     tr(2, d, (int64_t)ds.pend.len);
@@ -178,6 +284,14 @@ struct Worker {
     ds.used = true;
   }
   void write_value(int d, uint64_t off, uint64_t value) {
+    if (sm_engine) {
+      PJob& J = job_for(d, false);
+      J.sig[J.nsig] = reinterpret_cast<uint64_t*>(ctx->peer[d] + off);
+      J.val[J.nsig] = value;
+      ++J.nsig;
+      px->atomics.fetch_add(1, std::memory_order_relaxed);
+      return;
+    }
     DestState& ds = dest(d);
     WriteValue64Fn fn = write_value64();
     if (!fn) {
@@ -205,10 +319,16 @@ struct Worker {
         write_value(d, offsetof(epb::Meta, proxy_sig) + sizeof(uint64_t) * idx, ds.sig[k]);
       }
     }
+    if (sm_engine && !jobs.empty()) launch_jobs();
   }
   // events on every stream used since the last call (one completion point)
   std::vector<cudaEvent_t> mark_streams(bool all) {
     std::vector<cudaEvent_t> evs;
+    if (sm_engine && (kst_used || all)) {
+      cudaEvent_t ev = event();
+      if (ok(cudaEventRecord(ev, kst))) evs.push_back(ev);
+      kst_used = false;
+    }
     for (int d = 0; d < ctx->world; ++d) {
       DestState& ds = dests[d];
       if (!ds.st || !(ds.used || all)) continue;
@@ -331,7 +451,8 @@ struct Worker {
     const int C = ctx->cfg.fifo_channels;
     const int64_t cap = ctx->cfg.fifo_capacity, mask = cap - 1;
     dests.resize(ctx->world);
-    for (int ch = tid; ch < C; ch += nthreads) {
+    for (int ch = 0; ch < C; ++ch) {
+      if (epb::proxy_thread_of(ch, half, nthreads, ctx->proxy_chmap) != tid) continue;
       ChanState cs;
       cs.ch = ch;
       cs.head = load_acquire(&ctx->fifo_host[ch][EPB_CTL_HEAD]);
@@ -345,6 +466,26 @@ struct Worker {
     // The same holds for the first value write to a peer mapping (its first
     // LL call stalled for seconds at EP=2 until both paths were warmed here).
     const size_t probe = epb::kMetaBytes + offsetof(epb::Scratch, trace) + sizeof(int64_t) * 62;
+    // transfer engine: SM copy kernels by default (EP=4: LL pair 121 against 138 us,
+    // HT proxy dispatch / combine 492 / 541 against 594 / 717 us with the copy
+    // engine; profiles/r02_proxy_engine_n4.txt); EPB_PROXY_ENGINE=ce selects the
+    // copy engine (cudaMemcpyAsync + cuStreamWriteValue64)
+    sm_engine = true;
+    if (const char* e = std::getenv("EPB_PROXY_ENGINE")) sm_engine = std::strcmp(e, "ce") != 0;
+    if (sm_engine) {  // the copy-kernel stream, its tickets, and one warm-up launch
+      ok(cudaStreamCreateWithFlags(&kst, cudaStreamNonBlocking));
+      if (ok(cudaMalloc(&tickets, sizeof(uint32_t) * kPcopyJobs))) ok(cudaMemset(tickets, 0, sizeof(uint32_t) * kPcopyJobs));
+      if (tracing && ok(cudaMalloc(&stamps, sizeof(int64_t) * 2 * kStampRing)))
+        ok(cudaMemset(stamps, 0, sizeof(int64_t) * 2 * kStampRing));
+      PJob w;
+      w.dest = ctx->rank;
+      w.segs.push_back({ctx->base + probe, ctx->base + probe + 16, 16});
+      w.bytes = 16;
+      jobs.push_back(w);
+      launch_jobs();
+      ok(cudaStreamSynchronize(kst));
+      kst_used = false;
+    }
     for (int d = 0; d < ctx->world; ++d) {
       if (!ctx->peer[d]) continue;
       DestState& ds = dest(d);
@@ -448,6 +589,20 @@ struct Worker {
     for (cudaEvent_t ev : pool) cudaEventDestroy(ev);
     for (DestState& ds : dests)
       if (ds.st) cudaStreamDestroy(ds.st);
+    if (kst) {
+      cudaStreamSynchronize(kst);
+      cudaStreamDestroy(kst);
+    }
+    if (stamps) {  // device stamps (GPU clock) as trace kinds 10 (copy kernel start) / 11 (last signal)
+      std::vector<int64_t> h(2 * kStampRing);
+      if (cudaMemcpy(h.data(), stamps, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost) == cudaSuccess)
+        for (int i = 0; i < kStampRing; ++i) {
+          if (h[2 * i]) trace.push_back({h[2 * i], 10, tid, i});
+          if (h[2 * i + 1]) trace.push_back({h[2 * i + 1], 11, tid, i});
+        }
+      cudaFree(stamps);
+    }
+    if (tickets) cudaFree(tickets);
     std::lock_guard<std::mutex> g(px->trace_m);
     px->trace.insert(px->trace.end(), trace.begin(), trace.end());
   }

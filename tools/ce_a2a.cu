@@ -7,6 +7,9 @@
 //   C  one stream: copy, signal, copy, signal, ...
 //   D  receiver pull: one stream on the receiver copies from every peer, then
 //      one local signal
+//   K  SM copy kernel: one launch per GPU copies to every peer (blocks split
+//      each peer's bytes) and the last block per peer writes its signal
+//   L  as K, one launch per peer
 // Signals go to pinned host memory (cuStreamWriteValue64), so times include
 // ~1 us of PCIe write.
 //   nvcc -O2 -gencode arch=compute_100a,code=sm_100a tools/ce_a2a.cu -o /tmp/ce_a2a -lpthread
@@ -32,6 +35,26 @@
 
 using WV64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 static WV64 wv;
+
+__global__ void kcopy(const int4* const* src, int4* const* dst, unsigned long long* const* flag, uint64_t it,
+                      uint64_t n16, int bpp, unsigned* tickets) {
+  const int p = blockIdx.x / bpp, b = blockIdx.x % bpp;
+  const uint64_t u0 = n16 * b / bpp, u1 = n16 * (b + 1) / bpp;
+  for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+    int4 v;
+    asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src[p] + u));
+    dst[p][u] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(&tickets[p], 1u) == (unsigned)bpp - 1) {
+      tickets[p] = 0;
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag[p]), "l"(it) : "memory");
+    }
+  }
+}
 
 static double now_us() {
   return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -74,7 +97,7 @@ int main(int argc, char** argv) {
   std::atomic<uint64_t> go{0};
   std::printf("# GPUs %d\n# mode bytes_per_peer median_us p90_us (max over GPUs of issue->all own signals seen)\n", G);
   for (size_t bytes : {size_t(64) << 10, size_t(512) << 10, size_t(1) << 20, size_t(2) << 20}) {
-    for (char mode : {'A', 'B', 'C', 'D'}) {
+    for (char mode : {'A', 'K', 'L'}) {
       const int reps = 60;
       std::vector<std::vector<double>> lat(G);
       uint64_t base_it = 0;
@@ -117,6 +140,35 @@ int main(int argc, char** argv) {
                 copy_to(j, g[i].st[0]);
                 sig(g[i].st[0], k++);
               }
+          } else if (mode == 'K' || mode == 'L') {
+            static thread_local const int4** d_src = nullptr;
+            static thread_local int4** d_dst = nullptr;
+            static thread_local unsigned long long** d_flag = nullptr;
+            static thread_local unsigned* d_tick = nullptr;
+            if (!d_src) {
+              CK(cudaMallocManaged(&d_src, sizeof(void*) * kMaxG));
+              CK(cudaMallocManaged(&d_dst, sizeof(void*) * kMaxG));
+              CK(cudaMallocManaged(&d_flag, sizeof(void*) * kMaxG));
+              CK(cudaMalloc(&d_tick, sizeof(unsigned) * kMaxG * kMaxG));
+              CK(cudaMemset(d_tick, 0, sizeof(unsigned) * kMaxG * kMaxG));
+              int q = 0;
+              for (int j = 0; j < G; ++j)
+                if (j != i) {
+                  d_src[q] = reinterpret_cast<const int4*>(g[i].buf + j * slot);
+                  d_dst[q] = reinterpret_cast<int4*>(g[j].buf + (kMaxG + i) * slot);
+                  d_flag[q] = reinterpret_cast<unsigned long long*>(dflags + i * kMaxG + q);
+                  ++q;
+                }
+              CK(cudaDeviceSynchronize());
+            }
+            const int bpp = std::max<int>(1, (int)(bytes >> 16));
+            if (mode == 'K') {
+              kcopy<<<bpp * (G - 1), 512, 0, g[i].st[0]>>>(d_src, d_dst, d_flag, it, bytes / 16, bpp, d_tick);
+            } else {
+              for (int q = 0; q < G - 1; ++q)
+                kcopy<<<bpp, 512, 0, g[i].st[q]>>>(d_src + q, d_dst + q, d_flag + q, it, bytes / 16, bpp, d_tick + kMaxG * (q + 1));
+            }
+            nsig = G - 1;
           } else {  // D: pull every peer's send slot for me into my recv slots
             for (int j = 0; j < G; ++j)
               if (j != i)

@@ -93,7 +93,9 @@ def main():
     ev = (C.c_int64 * (4 * max(1, n)))()
     lib.epb_proxy_trace(buf._rank.ctx, ev, n)
     evs = np.frombuffer(ev, np.int64)[: 4 * n].reshape(n, 4).copy()
-    evs[:, 0] += off.value  # host events on the GPU clock
+    host_ev = evs[:, 1] < 10  # kinds >= 10: device stamps (already on the GPU clock)
+    evs[host_ev, 0] += off.value  # host events on the GPU clock
+    evs = evs[np.argsort(evs[:, 0], kind="stable")]
     G = args.fifo_channels // 2
 
     def phases(m, start, stage, push0, wake, done, chan_lo):
@@ -114,6 +116,8 @@ def main():
                 "host_sees_tail": rel(tail[0, 0]) if len(tail) else None,
                 "first_copy_issued": rel(cp[0, 0]) if len(cp) else None,
                 "last_signal_issued": rel(sig[-1, 0]) if len(sig) else None,
+                "copy_kernel_start": rel(win[win[:, 1] == 10][0, 0]) if (win[:, 1] == 10).any() else None,
+                "copy_kernel_last_signal": rel(win[win[:, 1] == 11][-1, 0]) if (win[:, 1] == 11).any() else None,
                 "receiver_wakes": rel(m[wake]), "done": rel(m[done])}
 
     if calls and len(evs):  # alignment sanity (stderr): the last call's marks vs the nearest host events
