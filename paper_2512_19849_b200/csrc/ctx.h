@@ -85,7 +85,8 @@ constexpr int kPcopyJobs = 8, kPcopySegs = 16;  // small launch parameters (~0.7
 struct epb_pcopy_batch {
   int njobs, nsegs, nblocks;
   uint32_t* tickets;  // [kPcopyJobs] device counters, zero between launches
-  int64_t* stamp;     // tracing: [2] = %globaltimer at kernel start, at the last signal (or nullptr)
+  int64_t* stamp;     // tracing: [4] = %globaltimer at kernel start, last signal, last block start,
+                      // last block's copies done (or nullptr)
   epb_pcopy_job jobs[kPcopyJobs];
   epb_pcopy_seg segs[kPcopySegs];
 };

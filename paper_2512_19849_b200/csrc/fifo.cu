@@ -20,7 +20,11 @@ namespace epb {
 // block of the job (a ticket) publishes its signal with st.release.sys after a
 // fence that orders every block's copies (release fence + relaxed RMW pattern).
 __global__ void __launch_bounds__(512) pcopy_kernel(const __grid_constant__ epb_pcopy_batch B) {
-  if (B.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) B.stamp[0] = (int64_t)globaltimer();
+  if (B.stamp != nullptr && threadIdx.x == 0) {
+    const unsigned long long now = globaltimer();
+    if (blockIdx.x == 0) B.stamp[0] = (int64_t)now;
+    atomicMax(reinterpret_cast<unsigned long long*>(&B.stamp[2]), now);  // the last block to start
+  }
   int j = 0;
   while (j + 1 < B.njobs && (int)blockIdx.x >= B.jobs[j + 1].block0) ++j;
   const epb_pcopy_job& J = B.jobs[j];
@@ -53,6 +57,7 @@ __global__ void __launch_bounds__(512) pcopy_kernel(const __grid_constant__ epb_
   if (J.sig == nullptr) return;
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (B.stamp != nullptr) atomicMax(reinterpret_cast<unsigned long long*>(&B.stamp[3]), (unsigned long long)globaltimer());
     fence_sys();
     if (atomicAdd(&B.tickets[j], 1u) == (uint32_t)nbj - 1) {
       B.tickets[j] = 0;

@@ -148,6 +148,7 @@ struct Worker {
   uint32_t* tickets = nullptr;    // SM engine: per-job last-block tickets (device)
   int64_t* stamps = nullptr;      // SM engine + tracing: [kStampRing][2] device stamps per launch
   int64_t launches = 0;
+  int64_t pcopy_block = 65536;    // SM engine: bytes per copy-kernel block (EPB_PCOPY_BLOCK_KB)
   static constexpr int kStampRing = 512;
   std::vector<PJob> jobs;         // SM engine: the sweep's open jobs, in issue order
   std::vector<ChanState> chans;
@@ -202,7 +203,7 @@ struct Worker {
   // one copy-kernel launch for the open jobs (several if they exceed a batch)
   int64_t* next_stamp() {
     if (!stamps) return nullptr;
-    int64_t* p = stamps + 2 * (launches % kStampRing);
+    int64_t* p = stamps + 4 * (launches % kStampRing);
     ++launches;
     return p;
   }
@@ -224,7 +225,10 @@ struct Worker {
         q.seg0 = b.nsegs;
         q.nseg = (int)J.segs.size();
         for (const epb_pcopy_seg& g : J.segs) b.segs[b.nsegs++] = g;
-        q.blocks = (int)std::min<uint64_t>(32, std::max<uint64_t>(1, J.bytes >> 16));
+        // one block per pcopy_block bytes (64 KB: LL pair 126 us at EP=4; 32 / 16 / 8 KB:
+        // 137 / 140 / 140 us — the extra blocks cannot all sit beside the LL kernel's and
+        // start in a second wave; profiles/r02_proxy_engine_n4.txt)
+        q.blocks = (int)std::min<uint64_t>(148, std::max<uint64_t>(1, J.bytes / (uint64_t)pcopy_block));
         q.block0 = b.nblocks;
         b.nblocks += q.blocks;
         q.sig = J.nsig > 0 ? J.sig[0] : nullptr;
@@ -472,11 +476,12 @@ struct Worker {
     // copy engine (cudaMemcpyAsync + cuStreamWriteValue64)
     sm_engine = true;
     if (const char* e = std::getenv("EPB_PROXY_ENGINE")) sm_engine = std::strcmp(e, "ce") != 0;
+    if (const char* e = std::getenv("EPB_PCOPY_BLOCK_KB")) pcopy_block = std::max<int64_t>(1, std::atoll(e)) << 10;
     if (sm_engine) {  // the copy-kernel stream, its tickets, and one warm-up launch
       ok(cudaStreamCreateWithFlags(&kst, cudaStreamNonBlocking));
       if (ok(cudaMalloc(&tickets, sizeof(uint32_t) * kPcopyJobs))) ok(cudaMemset(tickets, 0, sizeof(uint32_t) * kPcopyJobs));
-      if (tracing && ok(cudaMalloc(&stamps, sizeof(int64_t) * 2 * kStampRing)))
-        ok(cudaMemset(stamps, 0, sizeof(int64_t) * 2 * kStampRing));
+      if (tracing && ok(cudaMalloc(&stamps, sizeof(int64_t) * 4 * kStampRing)))
+        ok(cudaMemset(stamps, 0, sizeof(int64_t) * 4 * kStampRing));
       PJob w;
       w.dest = ctx->rank;
       w.segs.push_back({ctx->base + probe, ctx->base + probe + 16, 16});
@@ -594,12 +599,12 @@ struct Worker {
       cudaStreamDestroy(kst);
     }
     if (stamps) {  // device stamps (GPU clock) as trace kinds 10 (copy kernel start) / 11 (last signal)
-      std::vector<int64_t> h(2 * kStampRing);
+      // kinds 10: kernel start, 11: last signal, 12: last block start, 13: last block's copies done
+      std::vector<int64_t> h(4 * kStampRing);
       if (cudaMemcpy(h.data(), stamps, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost) == cudaSuccess)
-        for (int i = 0; i < kStampRing; ++i) {
-          if (h[2 * i]) trace.push_back({h[2 * i], 10, tid, i});
-          if (h[2 * i + 1]) trace.push_back({h[2 * i + 1], 11, tid, i});
-        }
+        for (int i = 0; i < kStampRing; ++i)
+          for (int q = 0; q < 4; ++q)
+            if (h[4 * i + q]) trace.push_back({h[4 * i + q], 10 + q, tid, i});
       cudaFree(stamps);
     }
     if (tickets) cudaFree(tickets);

@@ -117,6 +117,8 @@ def main():
                 "first_copy_issued": rel(cp[0, 0]) if len(cp) else None,
                 "last_signal_issued": rel(sig[-1, 0]) if len(sig) else None,
                 "copy_kernel_start": rel(win[win[:, 1] == 10][0, 0]) if (win[:, 1] == 10).any() else None,
+                "copy_kernel_last_block_start": rel(win[win[:, 1] == 12][-1, 0]) if (win[:, 1] == 12).any() else None,
+                "copy_kernel_copies_done": rel(win[win[:, 1] == 13][-1, 0]) if (win[:, 1] == 13).any() else None,
                 "copy_kernel_last_signal": rel(win[win[:, 1] == 11][-1, 0]) if (win[:, 1] == 11).any() else None,
                 "receiver_wakes": rel(m[wake]), "done": rel(m[done])}
 
