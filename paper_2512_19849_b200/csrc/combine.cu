@@ -640,13 +640,15 @@ __device__ __forceinline__ void combine_body(const CombineParams& P, uint32_t ep
   const bool abort = scratch_of(rv.base)->abort != 0;
   trace_mark(rv, 16);
 
-  if (P.stream == 1 && R > 1 && !abort) {
-    combine_stream<kMaxFan>(P, lr, s_cnt, s_excl, s_sendpre, s_mypre, epoch, par);
-    trace_mark(rv, 19);
-    trace_mark_max(rv, 20);
-    __syncthreads();
-    if (tid < R) bump_done(rv, tid, me);  // keeps the cumulative done counters in step (no wait)
-    return;
+  if constexpr (kMaxFan > 1) {  // (the one-rank instantiation never streams)
+    if (P.stream == 1 && R > 1 && !abort) {
+      combine_stream<kMaxFan>(P, lr, s_cnt, s_excl, s_sendpre, s_mypre, epoch, par);
+      trace_mark(rv, 19);
+      trace_mark_max(rv, 20);
+      __syncthreads();
+      if (tid < R) bump_done(rv, tid, me);  // keeps the cumulative done counters in step (no wait)
+      return;
+    }
   }
   // mode exchange: if every rank's combine input (and weights) lives inside its
   // symmetric region — e.g. the zero-copy recv_x of the dispatch — tokens are
@@ -692,13 +694,15 @@ __device__ __forceinline__ void combine_body(const CombineParams& P, uint32_t ep
   __syncthreads();
   bool pull = !P.force_push;
   for (int d = 0; d < R; ++d) pull = pull && s_xoff[d] >= 0;
-  if (!pull && !abort && P.stream == 2) {  // some input outside its region: streamed push
-    combine_stream<kMaxFan>(P, lr, s_cnt, s_excl, s_sendpre, s_mypre, epoch, par);
-    trace_mark(rv, 19);
-    trace_mark_max(rv, 20);
-    __syncthreads();
-    if (tid < R) bump_done(rv, tid, me);
-    return;
+  if constexpr (kMaxFan > 1) {
+    if (!pull && !abort && P.stream == 2) {  // some input outside its region: streamed push
+      combine_stream<kMaxFan>(P, lr, s_cnt, s_excl, s_sendpre, s_mypre, epoch, par);
+      trace_mark(rv, 19);
+      trace_mark_max(rv, 20);
+      __syncthreads();
+      if (tid < R) bump_done(rv, tid, me);
+      return;
+    }
   }
 
   // phase A (push mode): push rows back to their sources

@@ -83,7 +83,6 @@ struct DispatchParams {
   int tma;                      // rows move through per-warp shared-memory rings with bulk copies
   int tma_seg;                  // bytes per bulk unit (a row, or a part of it)
   int tma_smem_off;             // byte offset of the rings in dynamic shared memory
-  int64_t prefetch;             // bytes of its channel's source rows each block sends towards L2 at entry
   uint64_t ht_calls[kMaxLocal];  // proxy transport: expected ht_sig[0][src] (calls so far)
   uint32_t host_seq[kMaxLocal];  // tag of this call's host words (the host's call counter); the
                                  // mailbox epoch and done targets are device-resident (norm_call_begin)
@@ -444,23 +443,6 @@ __global__ void __launch_bounds__(kDispatchThreads, 1) dispatch_kernel(const __g
   __shared__ int s_abort;
   __shared__ uint32_t s_epoch, s_target;
   trace_mark(rv, 0);
-  if (tid == 32 && P.prefetch > 0) {
-    // start the channel's source rows towards L2 now (cp.async.bulk.prefetch):
-    // the count / plan phase below keeps the copy warps waiting for ~4 us, during
-    // which HBM would otherwise idle
-    const int Tc0 = P.solo ? (T + C - 2) / (C - 1) : (T + C - 1) / C;
-    const int t00 = P.solo ? (c == 0 ? 0 : (c - 1) * Tc0) : c * Tc0;
-    const int nt0 = (P.solo && c == 0) ? 0 : max(0, min(T, t00 + Tc0) - t00);
-    const size_t rb = (size_t)a.hidden * a.elem_bytes;
-    const char* p = static_cast<const char*>(a.x) + (size_t)t00 * rb;
-    size_t left = min((size_t)nt0 * rb, (size_t)P.prefetch) & ~(size_t)15;
-    while (left > 0) {
-      const uint32_t n = (uint32_t)min(left, (size_t)65536);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(n) : "memory");
-      p += n;
-      left -= n;
-    }
-  }
   if (tid == 0) {
     s_abort = 0;
     norm_call_begin(rv, 0, gridDim.x, &s_epoch, &s_target);
@@ -879,13 +861,6 @@ static int dispatch_launch(epb_t* const* ctxs, int n_local, const epb_dispatch_a
   }
   size_t smem = sizeof(int32_t) * (size_t)max_tc * ctxs[0]->world;
   if (smem > 160 * 1024) return epb_set_error(EPB_ERR_CONFIG, "too many tokens per channel; raise num_sms");
-  // L2 prefetch of each channel's source rows at kernel entry (EPB_DISPATCH_PREFETCH
-  // = bytes per block, 0 = off)
-  static const int64_t pf_env = [] {
-    const char* v = std::getenv("EPB_DISPATCH_PREFETCH");
-    return v ? (int64_t)std::atoll(v) : (int64_t)-1;
-  }();
-  P.prefetch = pf_env >= 0 ? pf_env : 0;
   // Bulk-copy rows (TMA engine) when the dispatch runs on a small SM budget:
   // at 20 / 24 / 48 channels it moves the DS-V3 rows 11-13 % faster than the
   // warp copy; on the whole GPU the warp copy wins the step (the combine behind
