@@ -77,7 +77,7 @@ struct epb_pcopy_seg {
   uint64_t len;
 };
 struct epb_pcopy_job {
-  int seg0, nseg, blocks, block0;
+  int dest, seg0, nseg, blocks, block0;
   uint64_t* sig;      // nullptr: no signal
   uint64_t sig_val;
 };

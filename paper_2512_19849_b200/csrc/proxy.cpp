@@ -55,6 +55,7 @@
 #include <vector>
 
 #include "ctx.h"
+#include "pcopy_plan.h"
 
 namespace {
 struct TraceEv {
@@ -129,15 +130,6 @@ struct Inflight {
 
 // SM copy engine (EPB_PROXY_ENGINE=sm): a destination's pending copies and up
 // to two signals, turned into one job of the sweep's copy-kernel launch
-struct PJob {
-  int dest = -1;
-  std::vector<epb_pcopy_seg> segs;
-  uint64_t* sig[2] = {nullptr, nullptr};
-  uint64_t val[2] = {0, 0};
-  int nsig = 0;
-  uint64_t bytes = 0;
-};
-
 struct Worker {
   epb_proxy* px;
   epb_ctx* ctx;
@@ -148,7 +140,10 @@ struct Worker {
   uint32_t* tickets = nullptr;    // SM engine: per-job last-block tickets (device)
   int64_t* stamps = nullptr;      // SM engine + tracing: [kStampRing][2] device stamps per launch
   int64_t launches = 0;
-  int64_t pcopy_block = 65536;    // SM engine: bytes per copy-kernel block (EPB_PCOPY_BLOCK_KB)
+  // SM engine: bytes per copy-kernel block (EPB_PCOPY_BLOCK_KB).  64 KB: LL pair 126 us
+  // at EP=4; 32 / 16 / 8 KB: 137 / 140 / 140 us — the extra blocks cannot all sit
+  // beside the LL kernel's and start in a second wave (profiles/r02_proxy_engine_n4.txt)
+  int64_t pcopy_block = 65536;
   static constexpr int kStampRing = 512;
   std::vector<PJob> jobs;         // SM engine: the sweep's open jobs, in issue order
   std::vector<ChanState> chans;
@@ -208,60 +203,13 @@ struct Worker {
     return p;
   }
   void launch_jobs() {
-    size_t i = 0;
-    while (i < jobs.size()) {
-      epb_pcopy_batch b;
-      std::memset(&b, 0, sizeof(b));
+    for (epb_pcopy_batch& b : pcopy_plan(jobs, pcopy_block)) {
       b.tickets = tickets;
       b.stamp = next_stamp();
-      // a destination's later job must not run beside its earlier one (its
-      // signal could overtake the earlier copies): one job per destination per launch
-      bool seen[epb::kMaxRanks] = {};
-      while (i < jobs.size() && b.njobs < kPcopyJobs && !seen[jobs[i].dest] &&
-             b.nsegs + (int)jobs[i].segs.size() <= kPcopySegs) {
-        const PJob& J = jobs[i];
-        seen[J.dest] = true;
-        epb_pcopy_job& q = b.jobs[b.njobs];
-        q.seg0 = b.nsegs;
-        q.nseg = (int)J.segs.size();
-        for (const epb_pcopy_seg& g : J.segs) b.segs[b.nsegs++] = g;
-        // one block per pcopy_block bytes (64 KB: LL pair 126 us at EP=4; 32 / 16 / 8 KB:
-        // 137 / 140 / 140 us — the extra blocks cannot all sit beside the LL kernel's and
-        // start in a second wave; profiles/r02_proxy_engine_n4.txt)
-        q.blocks = (int)std::min<uint64_t>(148, std::max<uint64_t>(1, J.bytes / (uint64_t)pcopy_block));
-        q.block0 = b.nblocks;
-        b.nblocks += q.blocks;
-        q.sig = J.nsig > 0 ? J.sig[0] : nullptr;
-        q.sig_val = J.val[0];
-        if (J.nsig > 0) tr(3, J.dest, (int64_t)J.val[0]);
-        ++b.njobs;
-        if (J.nsig == 2) {  // the second signal: a copy-free job right behind (next launch)
-          ++i;
-          tr(6, -1, (int64_t)b.nblocks);
-          ok(epb_pcopy_launch(b, kst));
-          std::memset(&b, 0, sizeof(b));
-          b.tickets = tickets;
-          b.stamp = next_stamp();
-          epb_pcopy_job& q2 = b.jobs[0];
-          q2.blocks = 1;
-          q2.sig = J.sig[1];
-          q2.sig_val = J.val[1];
-          tr(3, J.dest, (int64_t)J.val[1]);
-          b.njobs = 1;
-          b.nblocks = 1;
-          tr(6, -2, 1);
-          ok(epb_pcopy_launch(b, kst));
-          std::memset(&b, 0, sizeof(b));
-          b.tickets = tickets;
-          b.stamp = next_stamp();
-          break;
-        }
-        ++i;
-      }
-      if (b.njobs > 0) {
-        tr(6, -1, (int64_t)b.nblocks);
-        ok(epb_pcopy_launch(b, kst));
-      }
+      for (int j = 0; j < b.njobs; ++j)
+        if (b.jobs[j].sig) tr(3, b.jobs[j].dest, (int64_t)b.jobs[j].sig_val);
+      tr(6, -1, (int64_t)b.nblocks);
+      ok(epb_pcopy_launch(b, kst));
       px->copies.fetch_add(1, std::memory_order_relaxed);
       tr(2, -1, 0);
     }
