@@ -432,7 +432,7 @@ struct Worker {
         ok(cudaMemset(stamps, 0, sizeof(int64_t) * 4 * kStampRing));
       PJob w;
       w.dest = ctx->rank;
-      w.segs.push_back({ctx->base + probe, ctx->base + probe + 16, 16});
+      w.segs.push_back({ctx->base + probe, ctx->base + probe, 16});  // 16 bytes onto themselves
       w.bytes = 16;
       jobs.push_back(w);
       launch_jobs();
